@@ -1,0 +1,317 @@
+"""Throughput of the batched p-FHT-FSCL-L-M decoder on B200.
+
+Workload (BASELINE.json headline): RM(2,9), M=20 affine automorphisms
+(decoder 0's root maps = identity), L=4, BPSK/AWGN float32 LLRs at
+Eb/N0 = 2.5 dB.  One step = one decode launch over a batch of frames whose
+LLRs and permutation tables are resident in HBM (together larger than the
+126 MB L2, so no flush is needed between steps).
+
+  value     decoded frames/s of the whole job (sum over ranks / max time)
+  e2e       same metric through the public C-ABI path with host buffers:
+            pinned host LLRs + map records copied in, codewords/PM/attempt
+            copied out, every step
+  roofline  reference op ledger (accounting.complexity_model, include_perm)
+            per frame x frames/s against the FP32 issue peak
+            (SMs x 128 lanes x max SM clock); HBM bound alongside
+  cpu_baseline  the CPU oracle port (float64 restatement of the reference)
+            on this host's cores, bounded sample
+
+--impl reference times the CPU restatement of the reference decoder (the
+reference is pure Python with no native path; the oracle port is its CPU
+implementation here) on the same config, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+R, M_VARS, L, M = 2, 9, 4, 20
+EBN0 = 2.5
+WORKLOAD = "RM(2,9) p-FHT-FSCL L=4 M=20 (decoder 0 = identity), Eb/N0 2.5 dB"
+METRIC = "decoded frames/s, RM(2,9) M=20 L=4, 1 B200; % of roofline; vs host CPU"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d.get("hbm_gbs", 6536.4)), float(d.get("sm_max_mhz", 1965.0)), "measured"
+    except Exception:
+        return 6650.0, 1965.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 8
+                          for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_inputs(plan, spec, B, seed):
+    """Frames and permutation records for one batch (host)."""
+    from paper_2108_12550_b200.channel_model import synthetic_frames
+
+    x, llr = synthetic_frames(spec, EBN0, B, seed)
+    _, recs = plan.sample(B, seed, identity_root=True, want_raw=False)
+    return x, llr, recs
+
+
+def cpu_baseline(seconds: float = 12.0):
+    """Oracle port (float64 restatement) on all host cores over a bounded sample."""
+    from oracle import oracle
+    from paper_2108_12550_b200.channel_model import synthetic_frames
+    from paper_2108_12550_b200.plan import map_sizes
+    from paper_2108_12550_b200.automorphism import random_raw_table
+    from paper_2108_12550_b200.rm_core import build_code
+
+    spec = build_code(R, M_VARS)
+    cores = os.cpu_count() or 1
+    done, t_used, frames = 0, 0.0, 0
+    B = 16 * cores
+    while t_used < seconds and done < 64:
+        _, llr = synthetic_frames(spec, EBN0, B, 1000 + done)
+        raw = random_raw_table(np.random.default_rng(done), (B, M), map_sizes(R, M_VARS, L), M_VARS,
+                               identity_root=L)
+        t0 = time.perf_counter()
+        oracle.decode(R, M_VARS, L, M, llr, raw, dtype=np.float64, nthreads=cores, want_attempts=False)
+        t_used += time.perf_counter() - t0
+        frames += B
+        done += 1
+    return {"value": frames / t_used, "unit": "frames/s", "cores": cores, "kind": "port",
+            "sample": f"{frames} frames of the workload ({done} batches of {B}), float64 oracle port, "
+                      f"{cores} threads, {t_used:.1f} s"}
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    from oracle import oracle
+    from paper_2108_12550_b200.channel_model import synthetic_frames
+    from paper_2108_12550_b200.plan import map_sizes
+    from paper_2108_12550_b200.automorphism import random_raw_table
+    from paper_2108_12550_b200.rm_core import build_code
+
+    spec = build_code(R, M_VARS)
+    cores = os.cpu_count() or 1
+    B = 16 * cores
+    batches = []
+    for s in range(args.steps + args.warmup):
+        _, llr = synthetic_frames(spec, EBN0, B, 500 + s)
+        raw = random_raw_table(np.random.default_rng(s), (B, M), map_sizes(R, M_VARS, L), M_VARS, identity_root=L)
+        batches.append((llr, raw))
+    for llr, raw in batches[:args.warmup]:
+        oracle.decode(R, M_VARS, L, M, llr, raw, dtype=np.float64, nthreads=cores, want_attempts=False)
+    t0 = time.perf_counter()
+    for llr, raw in batches[args.warmup:]:
+        oracle.decode(R, M_VARS, L, M, llr, raw, dtype=np.float64, nthreads=cores, want_attempts=False)
+    dt = time.perf_counter() - t0
+    v = B * args.steps / dt
+    line = {"metric": METRIC, "value": v, "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": WORKLOAD, "frames_per_step": B},
+            "cpu_baseline": {"value": v, "unit": "frames/s", "cores": cores, "kind": "port",
+                             "sample": f"{B} frames per step x {args.steps} steps, float64 CPU restatement "
+                                       f"of the reference decoder (oracle/), {cores} threads"},
+            "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2108_12550_b200.decoder import Plan
+    from paper_2108_12550_b200.plan import complexity_ops
+    from paper_2108_12550_b200.rm_core import build_code
+
+    spec = build_code(R, M_VARS)
+    plan = Plan(R, M_VARS, L, M, True, "f32")
+    B = args.frames
+    x, llr, recs = make_inputs(plan, spec, B, seed=1 + rank)
+    dev = torch.device("cuda", local)
+    d_llr = torch.from_numpy(llr).to(dev)
+    d_rec = torch.from_numpy(recs.view(np.int16)).to(dev)
+    out = plan.alloc_outputs(B, dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        plan.launch(d_llr, d_rec, out, stream)
+    barrier()
+    # correctness spot check of the warm-up output (not timed)
+    cw = out["cw"].cpu().numpy().view(np.uint32)
+    bits = np.unpackbits(cw.view(np.uint8), axis=-1, bitorder="little")[:, :spec.N]
+    fer_warm = float(np.mean(np.any(bits != x, axis=1)))
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        time.sleep(0.3)
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            plan.launch(d_llr, d_rec, out, stream)
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = ws * B * args.steps / (ms / 1e3)
+
+    # e2e through the public path with host buffers, every step
+    h_llr = torch.from_numpy(llr).pin_memory()
+    h_rec = torch.from_numpy(recs.view(np.int16)).pin_memory()
+    h_cw = torch.empty(out["cw"].shape, dtype=torch.int32).pin_memory()
+    h_pm = torch.empty(out["pm"].shape, dtype=torch.float32).pin_memory()
+    h_att = torch.empty(out["attempt"].shape, dtype=torch.int32).pin_memory()
+    e_steps = max(1, min(args.steps, 5))
+
+    def e2e_step():
+        d_llr.copy_(h_llr, non_blocking=True)
+        d_rec.copy_(h_rec, non_blocking=True)
+        plan.launch(d_llr, d_rec, out, stream)
+        h_cw.copy_(out["cw"], non_blocking=True)
+        h_pm.copy_(out["pm"], non_blocking=True)
+        h_att.copy_(out["attempt"], non_blocking=True)
+
+    e2e_step()
+    barrier()
+    ev0.record(stream)
+    for _ in range(e_steps):
+        e2e_step()
+    ev1.record(stream)
+    barrier()
+    ms_e = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms_e], device=dev, dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_e = float(t.item())
+    e2e = ws * B * e_steps / (ms_e / 1e3)
+    h2d = llr.nbytes + recs.nbytes
+    d2h = h_cw.numel() * 4 + h_pm.numel() * 4 + h_att.numel() * 4
+
+    if rank == 0:
+        hbm, sm_mhz, src = _peaks()
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        ops = complexity_ops(R, M_VARS, L, M, True, include_perm=True)
+        peak_gops = sms * 128 * sm_mhz * 1e6 / 1e9
+        per_gpu = value / ws
+        ach_gops = ops * per_gpu / 1e9
+        bytes_frame = 4 * spec.N + spec.N // 8
+        rec_bytes_frame = M * plan.S * plan.rec_u16 * 2
+        clk = clk.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "frames_per_step": B, "parallelism": f"replicas{ws}",
+                       "l2": f"inputs {(llr.nbytes + recs.nbytes) / 2**20:.0f} MiB/step > 126 MB L2, no flush",
+                       "fer_check": fer_warm},
+            "e2e": {"value": e2e, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "steps": e_steps},
+            "gpu_launches": args.steps * plan.launches_per_call,
+            "roofline": {"bound": "fp32", "achieved": ach_gops, "peak": peak_gops, "unit": "Gop/s",
+                         "frac": ach_gops / peak_gops, "traffic": None,
+                         "ops_per_frame": ops,
+                         "note": f"reference op ledger x frames/s vs {sms} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz "
+                                 f"({src} sm_max_mhz)"},
+            "roofline_hbm": {"bound": "hbm", "achieved": (bytes_frame + rec_bytes_frame) * per_gpu / 1e9,
+                             "peak": hbm, "unit": "GB/s",
+                             "frac": (bytes_frame + rec_bytes_frame) * per_gpu / 1e9 / hbm,
+                             "bytes_per_frame": bytes_frame + rec_bytes_frame},
+            "clocks": clk,
+        }
+        if not args.no_cpu and ws == 1:
+            line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--frames", type=int, default=16384)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

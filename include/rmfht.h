@@ -1,0 +1,109 @@
+/*
+ * rmfht.h — C ABI of the B200 batched p-FHT-FSCL-L-M decoder
+ * (librmfht.so, paper_2108_12550_b200/csrc).
+ *
+ * The reference (arXiv 2108.12550 workbench, pkg/src/rmworkbench) is a pure
+ * Python package with no FFI; its boundary for this path is the Python
+ * function family in top_decoders.py, which this ABI replaces:
+ *
+ *   decode(spec, alpha, cfg, rng)                  top_decoders.py:252-271
+ *   ensemble_decode(spec, alpha, L, M, rng, sampler)  top_decoders.py:190-202
+ *   p_fht_fscl(spec, alpha, L, rng, sampler)       top_decoders.py:178-187
+ *   fht_fscl_decode / fht_fsc_decode               top_decoders.py:170-175
+ *   sampler: () -> AffinePermutation  (plugin hook, automorphism.py:225-226,
+ *                                      top_decoders.py:129-130)
+ *
+ * The Python mirror (paper_2108_12550_b200/top_decoders.py) binds these
+ * entry points with ctypes; INTEGRATION.md shows the binding.
+ *
+ * Conventions: all device pointers are caller-owned; launches are ordered on
+ * the given cudaStream_t (passed as void*) with no host synchronisation;
+ * plans are immutable after creation and may be shared between threads.
+ * Every function returns 0 on success and a negative code on error, with a
+ * one-line message from rmfht_last_error() (thread-local).
+ */
+#ifndef RMFHT_H
+#define RMFHT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rmfht_plan rmfht_plan;
+
+/* dtype: arithmetic of the decoder.  F32 is the throughput path; F64
+ * reproduces the float64 reference bit-for-bit. */
+enum { RMFHT_F32 = 0, RMFHT_F64 = 1 };
+
+/* flags */
+enum {
+    RMFHT_PERMUTATIONS = 1,   /* p-FHT-FSCL (else FHT-FSCL / FHT-FSC, M forced to 1) */
+    RMFHT_TIE_FIX = 2,        /* equal pairing directions keep equal LM (default for F32) */
+    RMFHT_NO_TIE_FIX = 4      /* force it off (default for F64) */
+};
+
+enum {
+    RMFHT_OK = 0,
+    RMFHT_ECONFIG = -1,       /* ConfigurationError (rm_core.py:72-77, top_decoders.py:38-42) */
+    RMFHT_EVALUE = -2,        /* ValueError: bad sizes / singular map (top_decoders.py:120-121) */
+    RMFHT_EUNSUPPORTED = -3,  /* valid configuration with no compiled kernel */
+    RMFHT_ECUDA = -4          /* CUDA runtime error */
+};
+
+/* Validate (r, m, L, M) like build_code + DecoderConfig and bind the kernel
+ * specialised on the static node schedule (accounting.plan_visits,
+ * accounting.py:96-123). */
+int rmfht_plan_create(int r, int m, int L, int M, int flags, int dtype, rmfht_plan **out);
+void rmfht_plan_destroy(rmfht_plan *plan);
+
+/* Permutation-table layout: S maps per attempt, in the reference's
+ * consumption order (L root maps, top_decoders.py:129-132; then 2L maps per
+ * permutation node, automorphism.py:224-228).  sizes[s] = variables of map s. */
+int rmfht_plan_maps_per_attempt(const rmfht_plan *plan);
+int rmfht_plan_map_sizes(const rmfht_plan *plan, int *sizes);
+int rmfht_plan_record_u16(const rmfht_plan *plan); /* 2m+2 */
+
+/* Host: convert `count` raw maps (m+1 uint16 each: row masks of A, bit j of
+ * row r = A[r, j] (automorphism.py:122-124), then b at index m) laid out as
+ * [.., S, m+1] into device records [.., S, 2m+2] (columns of A, b, columns
+ * of A^-1, A^-1 b).  Fails with RMFHT_EVALUE on a singular A. */
+int rmfht_expand_maps(const rmfht_plan *plan, const uint16_t *raw, uint16_t *rec, long long count);
+
+/* Host: sample the permutation table of frames frame0 .. frame0+B-1 —
+ * uniform (A, b) in GL(m_node, 2) x F_2^m_node per slot by rejection on
+ * random row masks (the reference's rule, automorphism.py:127-161), from a
+ * counter-based stream keyed by (seed, frame, attempt, slot), so a frame's
+ * maps do not depend on the batch it is drawn in.  identity_root != 0 makes
+ * attempt 0's L root maps the identity ("decoder 0 = identity").  Writes raw
+ * maps [B, M, S, m+1] and/or device records [B, M, S, 2m+2] (either may be
+ * NULL).  Multithreaded (OpenMP). */
+int rmfht_sample_maps(const rmfht_plan *plan, uint64_t seed, long long frame0, long long B,
+                      int identity_root, uint16_t *raw, uint16_t *rec);
+
+/* Decode B frames.  d_llr [B, 2^m] float or double (per dtype); d_maps
+ * [B, M, S, 2m+2] records (ignored without RMFHT_PERMUTATIONS); outputs
+ * d_cw [B, max(1, 2^m/32)] bit-packed codewords (bit i%32 of word i/32),
+ * d_pm [B] (dtype), d_attempt [B] selected attempt (first strict minimum,
+ * top_decoders.py:200), d_path [B] selected path within it (:152). */
+int rmfht_decode_launch(const rmfht_plan *plan, const void *d_llr, const uint16_t *d_maps,
+                        uint32_t *d_cw, void *d_pm, int32_t *d_attempt, int32_t *d_path,
+                        long long B, void *stream);
+
+/* As above, also writing every attempt's (pm, codeword): d_att_pm [B, M],
+ * d_att_cw [B, M, max(1, 2^m/32)] (either may be NULL). */
+int rmfht_decode_launch_diag(const rmfht_plan *plan, const void *d_llr, const uint16_t *d_maps,
+                             uint32_t *d_cw, void *d_pm, int32_t *d_attempt, int32_t *d_path,
+                             void *d_att_pm, uint32_t *d_att_cw, long long B, void *stream);
+
+/* Kernel launches per rmfht_decode_launch call (for the bench's launch count). */
+int rmfht_plan_launches_per_call(const rmfht_plan *plan);
+
+const char *rmfht_last_error(void);
+int rmfht_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RMFHT_H */

@@ -1,0 +1,83 @@
+// Kernel-binding unit: instantiates decode_kernel<T, r, m, L> for one dtype
+// and one chunk of RMFHT_CONFIGS; built once per (RMFHT_T, RMFHT_CHUNK).
+#include "rmfht_kernels.cuh"
+#include "rmfht_plan.h"
+
+#ifndef RMFHT_T
+#define RMFHT_T float
+#endif
+#ifndef RMFHT_CHUNK
+#define RMFHT_CHUNK 0
+#endif
+
+#define CHUNK_MACRO_(n) RMFHT_CHUNK##n
+#define CHUNK_MACRO(n) CHUNK_MACRO_(n)
+#define BINDER_(t, n) rmfht_bind_##t##_##n
+#define BINDER(t, n) BINDER_(t, n)
+
+using rmfht_internal::fail;
+
+namespace {
+
+template <typename T, int R, int MM, int L>
+int launch_impl(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint32_t* cw, void* pm,
+                int32_t* att, int32_t* path, void* att_pm, uint32_t* att_cw, long long B, cudaStream_t st) {
+    rmfht::Params<T> prm;
+    prm.llr = static_cast<const T*>(llr);
+    prm.maps = maps;
+    prm.B = B;
+    prm.M = p->M;
+    prm.perms = p->perms;
+    prm.tie_fix = p->tie_fix;
+    prm.cw = cw;
+    prm.pm = static_cast<T*>(pm);
+    prm.attempt = att;
+    prm.path = path;
+    prm.att_pm = static_cast<T*>(att_pm);
+    prm.att_cw = att_cw;
+    if (B <= 0) return 0;
+    auto* mp = const_cast<rmfht_plan*>(p);
+    std::call_once(mp->once, [mp] { mp->prepared_rc = mp->prepare(mp); });
+    if (p->prepared_rc != 0) return p->prepared_rc;
+    const long long grid = B < p->grid ? B : p->grid;
+    rmfht::decode_kernel<T, R, MM, L><<<(unsigned)grid, p->nwarps * 32, p->smem, st>>>(prm);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(RMFHT_ECUDA, std::string("decode launch: ") + cudaGetErrorString(e));
+    return 0;
+}
+
+template <typename T, int R, int MM, int L>
+int prepare(rmfht_plan* p) {
+    const int Meff = p->perms ? p->M : 1;
+    int nw = Meff < 8 ? Meff : 8;
+    if (nw < 1) nw = 1;
+    // keep a CTA's shared memory under ~110 KB so two CTAs fit an SM
+    while (nw > 1 && rmfht::smem_bytes<T, R, MM, L>(nw) > 110 * 1024) nw--;
+    const size_t smem = rmfht::smem_bytes<T, R, MM, L>(nw);
+    auto kern = rmfht::decode_kernel<T, R, MM, L>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(RMFHT_ECUDA, std::string("smem attribute: ") + cudaGetErrorString(e));
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem);
+    if (e != cudaSuccess || per_sm < 1) return fail(RMFHT_ECUDA, "kernel does not fit an SM");
+    p->nwarps = nw;
+    p->smem = smem;
+    p->grid = sms * per_sm;
+    return 0;
+}
+
+}  // namespace
+
+int BINDER(RMFHT_T, RMFHT_CHUNK)(rmfht_plan* p) {
+#define X(R_, M_, L_)                                          \
+    if (p->r == R_ && p->m == M_ && p->L == L_) {              \
+        p->launch = &launch_impl<RMFHT_T, R_, M_, L_>;         \
+        p->prepare = &prepare<RMFHT_T, R_, M_, L_>;            \
+        return 0;                                              \
+    }
+    CHUNK_MACRO(RMFHT_CHUNK)(X)
+#undef X
+    return RMFHT_EUNSUPPORTED;
+}

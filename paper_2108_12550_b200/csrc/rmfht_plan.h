@@ -1,0 +1,49 @@
+// Internal plan object shared by the C-ABI unit and the kernel-binding units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/rmfht.h"
+
+using LaunchFn = int (*)(const rmfht_plan*, const void*, const uint16_t*, uint32_t*, void*, int32_t*,
+                         int32_t*, void*, uint32_t*, long long, cudaStream_t);
+using PrepareFn = int (*)(rmfht_plan*);
+
+struct rmfht_plan {
+    int r, m, L, M, perms, tie_fix, dtype;
+    int S, nwarps, grid;
+    size_t smem;
+    std::vector<int> sizes;
+    LaunchFn launch;
+    PrepareFn prepare;  // CUDA-side binding (shared memory, occupancy), once at the first launch
+    std::once_flag once;
+    int prepared_rc;
+};
+
+namespace rmfht_internal {
+int fail(int code, const std::string& msg);
+}
+
+// Specialisations compiled into this library: (r, m, L), each for float and
+// double.  BASELINE.json's configurations plus the shapes the reference's
+// tests exercise.  Split into chunks that compile in
+// parallel (rmfht_bind.cu is built once per dtype x chunk).
+#define RMFHT_CHUNK0(X) X(2, 9, 4) X(2, 5, 1) X(1, 2, 4) X(3, 4, 4)
+#define RMFHT_CHUNK1(X) X(3, 7, 8) X(2, 4, 2) X(1, 5, 4)
+#define RMFHT_CHUNK2(X) X(2, 9, 1) X(2, 7, 2) X(2, 6, 4) X(2, 6, 1)
+#define RMFHT_CHUNK3(X) X(2, 8, 8) X(3, 8, 4) X(2, 9, 2) X(3, 6, 2) X(2, 5, 4)
+#define RMFHT_NCHUNKS 4
+
+// one binder per (dtype, chunk): returns RMFHT_EUNSUPPORTED when no match
+#define RMFHT_DECL_BINDERS(T)              \
+    int rmfht_bind_##T##_0(rmfht_plan* p); \
+    int rmfht_bind_##T##_1(rmfht_plan* p); \
+    int rmfht_bind_##T##_2(rmfht_plan* p); \
+    int rmfht_bind_##T##_3(rmfht_plan* p);
+RMFHT_DECL_BINDERS(float)
+RMFHT_DECL_BINDERS(double)

@@ -1,0 +1,75 @@
+"""The C-ABI library: loads, exports include/rmfht.h, validates like the
+reference, expands maps like the oracle.  No GPU compute here."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from paper_2108_12550_b200 import _native
+from paper_2108_12550_b200.automorphism import random_raw_table
+from paper_2108_12550_b200.plan import map_sizes
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "rmfht.h")).read()
+    return sorted(set(re.findall(r"\b(rmfht_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _native.lib()
+    declared = _declared()
+    assert set(declared) == set(_native.EXPORTS)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.rmfht_version() >= 1
+
+
+def _create(r, m, L, M, flags=1, dtype=0):
+    lib = _native.lib()
+    h = ctypes.c_void_p()
+    rc = lib.rmfht_plan_create(r, m, L, M, flags, dtype, ctypes.byref(h))
+    return rc, h
+
+
+@pytest.mark.parametrize("r,m,L,M,code", [(0, 5, 1, 1, -1), (5, 5, 1, 1, -1), (2, 15, 1, 1, -1),
+                                          (2, 9, 0, 1, -1), (2, 9, 4, 0, -1), (2, 9, 3, 5, -3)])
+def test_plan_create_errors(r, m, L, M, code):
+    rc, h = _create(r, m, L, M)
+    assert rc == code and not h.value
+    assert _native.last_error()
+
+
+def test_plan_layout_matches_host_schedule():
+    lib = _native.lib()
+    for (r, m, L, M) in [(2, 9, 4, 20), (3, 7, 8, 32), (2, 9, 1, 512), (2, 7, 2, 4)]:
+        rc, h = _create(r, m, L, M)
+        assert rc == 0, _native.last_error()
+        S = lib.rmfht_plan_maps_per_attempt(h)
+        sizes = (ctypes.c_int * S)()
+        lib.rmfht_plan_map_sizes(h, sizes)
+        assert list(sizes) == map_sizes(r, m, L)
+        assert lib.rmfht_plan_record_u16(h) == 2 * m + 2
+        lib.rmfht_plan_destroy(h)
+
+
+def test_expand_maps_matches_oracle(oracle_mod):
+    lib = _native.lib()
+    r, m, L = 3, 7, 8
+    rc, h = _create(r, m, L, 4)
+    sizes = map_sizes(r, m, L)
+    raw = random_raw_table(np.random.default_rng(3), (3, 4), sizes, m)
+    rec = np.zeros(raw.shape[:-1] + (2 * m + 2,), dtype=np.uint16)
+    assert lib.rmfht_expand_maps(h, raw.ctypes.data, rec.ctypes.data, raw.size // (m + 1)) == 0
+    rec2 = np.zeros_like(rec)
+    sz = np.asarray(sizes, dtype=np.int32)
+    assert oracle_mod.lib().rmo_expand_table(raw.ctypes.data, raw.size // (m + 1), m, sz.ctypes.data,
+                                              len(sizes), rec2.ctypes.data) == 0
+    assert np.array_equal(rec, rec2)
+    # a singular map is a ValueError-class error
+    raw[1, 2, 5, :] = 0
+    assert lib.rmfht_expand_maps(h, raw.ctypes.data, rec.ctypes.data, raw.size // (m + 1)) == -2
+    assert "invertible" in _native.last_error()
+    lib.rmfht_plan_destroy(h)

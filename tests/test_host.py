@@ -1,0 +1,79 @@
+"""Host-side logic: code shapes, schedule, map tables, sampler stream replay."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from paper_2108_12550_b200 import automorphism as aut
+from paper_2108_12550_b200.plan import map_sizes, plan_visits
+from paper_2108_12550_b200.rm_core import (ConfigurationError, build_code, is_codeword,
+                                           polar_transform, random_message)
+
+
+def test_build_code_shapes_and_errors():
+    s = build_code(2, 9)
+    assert (s.N, s.K, s.d) == (512, 46, 128)
+    assert build_code(3, 7).K == 64 and build_code(2, 7).K == 29 and build_code(2, 5).K == 16
+    for r, m in [(0, 5), (5, 5), (1, 1), (1, 15)]:
+        with pytest.raises(ConfigurationError):
+            build_code(r, m)
+
+
+def test_schedules_match_survey():
+    # SURVEY §3.3 probed schedules (accounting.plan_visits)
+    v = plan_visits(2, 9)
+    assert v[:3] == [("perm", 9), ("f", 9), ("fht", 8)]
+    assert v[-1] == ("spc", 3)
+    assert sum(1 for k, _ in v if k == "perm") == 1
+    v37 = plan_visits(3, 7)
+    assert [m for k, m in v37 if k == "perm"] == [7, 6]
+    assert sum(1 for k, _ in v37 if k == "fht") == 6 and sum(1 for k, _ in v37 if k == "spc") == 4
+    assert map_sizes(2, 9, 4) == [9] * 12
+    assert map_sizes(3, 7, 8) == [7] * 24 + [6] * 16
+    assert map_sizes(2, 9, 1) == [9] * 3
+    assert map_sizes(2, 5, 1, permutations=False) == []
+
+
+def test_polar_codewords():
+    rng = np.random.default_rng(0)
+    spec = build_code(2, 6)
+    for _ in range(20):
+        x = polar_transform(random_message(spec, rng))
+        assert is_codeword(spec, x)
+    x[3] ^= 1
+    assert not is_codeword(spec, x)
+
+
+def test_sampler_replays_reference_stream():
+    d = np.load(os.path.join(GOLDEN, "sampler_stream.npz"))
+    for key in [k for k in d.files if not k.endswith(("_next", "_perm0"))]:
+        m, count, seed = (int(t[1:]) for t in key.split("_"))
+        g = np.random.default_rng(seed)
+        maps = aut.sample_affine_batch(m, count, g)
+        assert np.array_equal(aut.maps_to_raw(maps, m), d[key])
+        assert np.array_equal(g.integers(0, 2 ** 31, size=4), d[key + "_next"])  # same draws consumed
+        assert np.array_equal(maps[0].perm, d[key + "_perm0"])
+
+
+def test_random_table_is_invertible_and_uniform_shape():
+    rng = np.random.default_rng(1)
+    sizes = map_sizes(3, 7, 8)
+    raw = aut.random_raw_table(rng, (5, 3), sizes, 7, identity_root=8)
+    assert raw.shape == (5, 3, len(sizes), 8)
+    for f in range(5):
+        for a in range(3):
+            for s, mn in enumerate(sizes):
+                masks = raw[f, a, s, :mn].astype(np.int64)
+                assert aut.gf2_invertible_masks(masks[None, :], mn)[0]
+                assert not raw[f, a, s, mn:7].any()
+    assert np.all(raw[:, 0, :8, :7] == (1 << np.arange(7)))
+    assert np.all(raw[:, 0, :8, 7] == 0)
+
+
+def test_affine_map_inverse_and_identity():
+    rng = np.random.default_rng(2)
+    for m in (3, 6, 9):
+        p = aut.sample_affine_batch(m, 1, rng)[0]
+        assert np.array_equal(p.perm[p.inv], np.arange(1 << m))
+    assert np.array_equal(aut.AffineMap.identity(4).perm, np.arange(16))

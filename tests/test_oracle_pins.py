@@ -1,0 +1,52 @@
+"""Pin the CPU oracle against the unmodified Python reference.
+
+tests/golden/*.npz were produced by tools/gen_golden.py, which ran the
+reference's own p_fht_fscl / ensemble_decode / fht_fsc(l)_decode on these
+exact LLRs and permutation tables.  The float64 oracle must match every
+field bit-for-bit; the float32 restatement must match exactly on
+exact-arithmetic fixtures and stay within the fp32 tolerance on channel
+fixtures.
+"""
+import numpy as np
+import pytest
+
+from conftest import golden_names, load_golden
+
+NAMES = golden_names()
+
+
+def _run(oracle_mod, g, dtype):
+    return oracle_mod.decode(g["r"], g["m"], g["L"], g["M"], g["llr"],
+                             g["raw"] if g["perms"] else None, perms=bool(g["perms"]),
+                             dtype=dtype, nthreads=4)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_f64_oracle_is_bit_exact_with_reference(oracle_mod, name):
+    g = load_golden(name)
+    o = _run(oracle_mod, g, np.float64)
+    assert np.array_equal(o["cw"], g["cw_bits"])
+    assert np.array_equal(o["pm"], g["pm"])
+    assert np.array_equal(o["attempt"], g["attempt"])
+    assert np.array_equal(o["att_pm"], g["att_pm"])
+    assert np.array_equal(o["att_cw"], g["att_cw_bits"])
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_f32_oracle_against_reference(oracle_mod, name):
+    g = load_golden(name)
+    o = _run(oracle_mod, g, np.float32)
+    if g["mode"] != "channel":
+        # integer LLRs: every intermediate is exact in float32
+        assert np.array_equal(o["cw"], g["cw_bits"])
+        assert np.array_equal(o["pm"].astype(np.float64), g["pm"])
+        assert np.array_equal(o["attempt"], g["attempt"])
+        assert np.array_equal(o["att_pm"].astype(np.float64), g["att_pm"])
+    else:
+        # PM within 1e-5 relative (absolute 1e-5 near zero), codewords equal
+        # except frames the f64 oracle marks as near-ties
+        pm = o["pm"].astype(np.float64)
+        assert np.all(np.abs(pm - g["pm"]) <= 1e-5 * np.maximum(np.abs(g["pm"]), 1.0))
+        o64 = _run(oracle_mod, g, np.float64)
+        differ = ~np.all(o["cw"] == g["cw_bits"], axis=1)
+        assert np.all(o64["margin"][differ] <= 1e-5)
