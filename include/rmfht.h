@@ -41,7 +41,9 @@ enum { RMFHT_F32 = 0, RMFHT_F64 = 1 };
 enum {
     RMFHT_PERMUTATIONS = 1,   /* p-FHT-FSCL (else FHT-FSCL / FHT-FSC, M forced to 1) */
     RMFHT_TIE_FIX = 2,        /* equal pairing directions keep equal LM (default for F32) */
-    RMFHT_NO_TIE_FIX = 4      /* force it off (default for F64) */
+    RMFHT_NO_TIE_FIX = 4,     /* force it off (default for F64) */
+    RMFHT_REFERENCE_ORDER = 8 /* F32: use the reference-operation-order kernel instead of the
+                                 throughput kernel (whose LM / llr_abs summation orders differ) */
 };
 
 enum {
@@ -99,6 +101,10 @@ int rmfht_decode_launch_diag(const rmfht_plan *plan, const void *d_llr, const ui
 
 /* Kernel launches per rmfht_decode_launch call (for the bench's launch count). */
 int rmfht_plan_launches_per_call(const rmfht_plan *plan);
+
+/* Which kernel the plan runs: 1 = reference-order (rmfht_kernels.cuh),
+ * 2 = float32 throughput kernel (rmfht_fast.cuh); 0 for a NULL plan. */
+int rmfht_plan_kernel(const rmfht_plan *plan);
 
 const char *rmfht_last_error(void);
 int rmfht_version(void);

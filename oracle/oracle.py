@@ -50,8 +50,11 @@ def maps_per_attempt(r, m, L, perms=True):
     return lib().rmo_maps_per_attempt(r, m, L, int(perms), None)
 
 
+RMO_TIE_FIX, RMO_ORDER_V2 = 1, 2
+
+
 def decode(r, m, L, M, llr, raw_maps=None, perms=True, dtype=np.float64, tie_fix=None,
-           nthreads=1, want_attempts=True):
+           nthreads=1, want_attempts=True, order="reference"):
     """Decode a batch on the CPU oracle.
 
     llr: (B, N) array; raw_maps: (B, M, S, m+1) uint16 or None when perms is
@@ -59,10 +62,13 @@ def decode(r, m, L, M, llr, raw_maps=None, perms=True, dtype=np.float64, tie_fix
     the same operation order in float32 (the GPU fp32 kernel's arithmetic).
     tie_fix defaults to on for float32 (equal pairing directions keep equal
     LM) and off for float64 (pure reference behaviour).
+    order="v2" restates the float32 throughput kernel's summation orders
+    (llr_abs and LM; canonical LM order makes the tie fix implicit).
     """
     dtype = np.dtype(dtype)
     if tie_fix is None:
-        tie_fix = dtype == np.float32
+        tie_fix = dtype == np.float32 and order != "v2"
+    flags = (RMO_TIE_FIX if tie_fix else 0) | (RMO_ORDER_V2 if order == "v2" else 0)
     llr = np.ascontiguousarray(llr, dtype=dtype)
     B, N = llr.shape
     if N != 1 << m:
@@ -81,7 +87,7 @@ def decode(r, m, L, M, llr, raw_maps=None, perms=True, dtype=np.float64, tie_fix
     att_cw = np.zeros((B, Meff, N), dtype=np.uint8) if want_attempts else None
     margin = np.zeros(B, dtype=np.float64)
     fn = lib().rmo_decode_f64 if dtype == np.float64 else lib().rmo_decode_f32
-    rc = fn(r, m, L, M, int(perms), int(bool(tie_fix)), _ptr(llr), B,
+    rc = fn(r, m, L, M, int(perms), flags, _ptr(llr), B,
             _ptr(raw_maps) if perms else None, int(nthreads), _ptr(cw), _ptr(pm), _ptr(att),
             _ptr(path), _ptr(att_pm), _ptr(att_cw), _ptr(margin))
     if rc != 0:

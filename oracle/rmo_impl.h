@@ -20,6 +20,7 @@
 
 typedef struct {
     int r, m, N, L, perms, tie_fix;
+    int v2;  /* RMO_ORDER_V2: the float32 throughput kernel's summation orders */
     const rmo_map *maps; /* this attempt's maps, in consumption order */
     int nmaps, next_map;
     int perm_active;        /* top_decoders.py:62,77-78 */
@@ -59,6 +60,94 @@ static inline void FN(note)(FN(rmo_ctx) *cx, double a, double b)
 {
     double g = rmo_rel_gap(a, b);
     if (g < cx->margin) cx->margin = g;
+}
+
+/* RMO_ORDER_V2 sum of |x| over a node of size n held by a lane group of lpp
+ * lanes (element e = k*lpp + u): per-lane partials in slot order, then the
+ * group tree with offsets 1, 2, 4, ... (rmfht_fast.cuh, fht_node). */
+static REAL FN(v2_group_sum)(const REAL *a, int n, int lpp)
+{
+    REAL q[32];
+    int act = n >= lpp ? lpp : n, V = n >= lpp ? n / lpp : 1;
+    for (int u = 0; u < act; u++) {
+        q[u] = a[u];
+        for (int k = 1; k < V; k++) q[u] += a[k * lpp + u];
+    }
+    for (int off = 1; off < act; off <<= 1) {
+        REAL t[32];
+        for (int u = 0; u < act; u++) t[u] = q[u] + q[u ^ off];
+        for (int u = 0; u < act; u++) q[u] = t[u];
+    }
+    return q[0];
+}
+
+/* RMO_ORDER_V2 32-lane tree (offsets 16, 8, 4, 2, 1), rmfht_fast.cuh multi_tree */
+static REAL FN(v2_lane_tree)(REAL *v)
+{
+    for (int off = 16; off >= 1; off >>= 1) {
+        REAL t[32];
+        for (int l = 0; l < 32; l++) t[l] = v[l] + v[l ^ off];
+        for (int l = 0; l < 32; l++) v[l] = t[l];
+    }
+    return v[0];
+}
+
+static int rmo_hibit(unsigned x) { return 31 - __builtin_clz(x); }
+
+/* RMO_ORDER_V2 LM at the root: pairs (i, i^d) of channel indices, lane l
+ * owning i = l + 32 s (rmfht_fast.cuh, lm_partial_root). */
+static REAL FN(v2_lm_root)(const REAL *alpha, int N, unsigned d)
+{
+    REAL v[32];
+    int NS = N / 32;
+    unsigned c = d >> 5, delta = d & 31;
+    for (int l = 0; l < 32; l++) {
+        REAL acc = 0;
+        int first = 1;
+        if (c != 0) {
+            int hb = rmo_hibit(c);
+            for (int s = 0; s < NS; s++) {
+                if (s >> hb & 1) continue;
+                unsigned i = (unsigned)(l + 32 * s);
+                REAL x = alpha[i] < 0 ? -alpha[i] : alpha[i], y = alpha[i ^ d] < 0 ? -alpha[i ^ d] : alpha[i ^ d];
+                REAL mn = y < x ? y : x;
+                acc = first ? mn : acc + mn;
+                first = 0;
+            }
+        } else {
+            int h = rmo_hibit(delta);
+            if (!((l >> h) & 1))
+                for (int s = 0; s < NS; s++) {
+                    unsigned i = (unsigned)(l + 32 * s);
+                    REAL x = alpha[i] < 0 ? -alpha[i] : alpha[i], y = alpha[i ^ d] < 0 ? -alpha[i ^ d] : alpha[i ^ d];
+                    REAL mn = y < x ? y : x;
+                    acc = first ? mn : acc + mn;
+                    first = 0;
+                }
+        }
+        v[l] = acc;
+    }
+    return FN(v2_lane_tree)(v);
+}
+
+/* RMO_ORDER_V2 LM at an inner permutation node: canonical pairs q = l + 32 r,
+ * i = q with a zero inserted at the top bit of d (perm_ext_inner2). */
+static REAL FN(v2_lm_inner)(const REAL *x, int n, unsigned d)
+{
+    REAL v[32];
+    int H = n / 2, h = rmo_hibit(d);
+    for (int l = 0; l < 32; l++) {
+        REAL acc = 0;
+        int r = 0;
+        for (int q = l; q < H; q += 32, r++) {
+            int i = ((q >> h) << (h + 1)) | (q & ((1 << h) - 1));
+            REAL a = x[i] < 0 ? -x[i] : x[i], b = x[i ^ (int)d] < 0 ? -x[i ^ (int)d] : x[i ^ (int)d];
+            REAL mn = b < a ? b : a;
+            acc = r == 0 ? mn : acc + mn;
+        }
+        v[l] = acc;
+    }
+    return FN(v2_lane_tree)(v);
 }
 
 /* f_op, list_engine.py:15-20: min(|a|,|b|) * sgn(a) * sgn(b), sgn(0)=+1 */
@@ -102,7 +191,7 @@ static int FN(fhtl)(FN(rmo_ctx) *cx, const REAL *alphas, int p, int n, REAL *pms
         const REAL *a = alphas + (size_t)row * n;
         REAL *wr = w + (size_t)row * n, *ar = absw + (size_t)row * n;
         for (int j = 0; j < n; j++) { wr[j] = a[j]; tmp[j] = a[j] < 0 ? -a[j] : a[j]; }
-        REAL llr_abs = FN(pw_sum)(tmp, n);                 /* :114 */
+        REAL llr_abs = cx->v2 ? FN(v2_group_sum)(tmp, n, 32 / L) : FN(pw_sum)(tmp, n); /* :114 */
         FN(fht)(wr, n);                                     /* :112 */
         for (int j = 0; j < n; j++) ar[j] = wr[j] < 0 ? -wr[j] : wr[j];
         /* stable argsort of -|w| → |w| descending, ties to the lower bin (:116) */
@@ -285,6 +374,8 @@ static int FN(perm_extend)(FN(rmo_ctx) *cx, const REAL *alphas, int p, int n, in
         unsigned d = mp[t].icol[mp[t].m - 1];
         if (is_root) key[t] = rmo_lin_inv(cx->init[src], d);
         else key[t] = (unsigned)src << 16 | d;
+        if (cx->v2) /* same multiset of pair minima, canonical order */
+            lm[t] = is_root ? FN(v2_lm_root)(cx->root_llr, cx->N, key[t]) : FN(v2_lm_inner)(a, n, d);
     }
     if (cx->tie_fix)
         for (int t = 1; t < trials; t++)
@@ -433,7 +524,7 @@ static int FN(attempt)(FN(rmo_ctx) *cx, const REAL *llr, uint8_t *cw, REAL *pm_o
 
 /* ensemble_decode, top_decoders.py:190-202, over a batch of frames.  With
  * perms == 0 this is fht_fscl_decode / fht_fsc_decode (one attempt, M = 1). */
-int FN(rmo_decode)(int r, int m, int L, int M, int perms, int tie_fix, const REAL *llr, long B,
+int FN(rmo_decode)(int r, int m, int L, int M, int perms, int flags, const REAL *llr, long B,
                    const uint16_t *raw_maps, int nthreads, uint8_t *cw_out, REAL *pm_out,
                    int32_t *attempt_out, int32_t *path_out, REAL *att_pm, uint8_t *att_cw,
                    double *margin_out)
@@ -455,7 +546,9 @@ int FN(rmo_decode)(int r, int m, int L, int M, int perms, int tie_fix, const REA
         uint8_t *cw = (uint8_t *)malloc((size_t)N);
         FN(rmo_ctx) cx;
         memset(&cx, 0, sizeof cx);
-        cx.r = r; cx.m = m; cx.N = N; cx.L = L; cx.perms = perms; cx.tie_fix = tie_fix;
+        cx.r = r; cx.m = m; cx.N = N; cx.L = L; cx.perms = perms;
+        cx.tie_fix = flags & RMO_TIE_FIX ? 1 : 0;
+        cx.v2 = flags & RMO_ORDER_V2 ? 1 : 0;
         cx.maps = maps; cx.nmaps = S; cx.ar = &ar;
 #ifdef _OPENMP
 #pragma omp for schedule(dynamic, 4)

@@ -17,7 +17,7 @@ CSRC = os.path.join(_HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(_HERE), "include")
 
 RMFHT_F32, RMFHT_F64 = 0, 1
-RMFHT_PERMUTATIONS, RMFHT_TIE_FIX, RMFHT_NO_TIE_FIX = 1, 2, 4
+RMFHT_PERMUTATIONS, RMFHT_TIE_FIX, RMFHT_NO_TIE_FIX, RMFHT_REFERENCE_ORDER = 1, 2, 4, 8
 RMFHT_OK, RMFHT_ECONFIG, RMFHT_EVALUE, RMFHT_EUNSUPPORTED, RMFHT_ECUDA = 0, -1, -2, -3, -4
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
@@ -27,7 +27,7 @@ EXPORTS = [
     "rmfht_plan_create", "rmfht_plan_destroy", "rmfht_plan_maps_per_attempt",
     "rmfht_plan_map_sizes", "rmfht_plan_record_u16", "rmfht_expand_maps",
     "rmfht_decode_launch", "rmfht_decode_launch_diag", "rmfht_plan_launches_per_call",
-    "rmfht_last_error", "rmfht_version", "rmfht_sample_maps",
+    "rmfht_last_error", "rmfht_version", "rmfht_sample_maps", "rmfht_plan_kernel",
 ]
 
 _lib = None
@@ -88,6 +88,8 @@ def lib():
     L.rmfht_plan_record_u16.restype = I
     L.rmfht_plan_launches_per_call.argtypes = [P]
     L.rmfht_plan_launches_per_call.restype = I
+    L.rmfht_plan_kernel.argtypes = [P]
+    L.rmfht_plan_kernel.restype = I
     L.rmfht_expand_maps.argtypes = [P, P, P, LL]
     L.rmfht_expand_maps.restype = I
     L.rmfht_decode_launch.argtypes = [P, P, P, P, P, P, P, LL, P]

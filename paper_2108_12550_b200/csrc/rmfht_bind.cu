@@ -1,5 +1,6 @@
 // Kernel-binding unit: instantiates decode_kernel<T, r, m, L> for one dtype
 // and one chunk of RMFHT_CONFIGS; built once per (RMFHT_T, RMFHT_CHUNK).
+#include "rmfht_fast.cuh"
 #include "rmfht_kernels.cuh"
 #include "rmfht_plan.h"
 
@@ -68,15 +69,72 @@ int prepare(rmfht_plan* p) {
     return 0;
 }
 
+template <int R, int MM, int L>
+int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint32_t* cw, void* pm, int32_t* att,
+                int32_t* path, void* att_pm, uint32_t* att_cw, long long B, cudaStream_t st) {
+    rmfht::Params<float> prm;
+    prm.llr = static_cast<const float*>(llr);
+    prm.maps = maps;
+    prm.B = B;
+    prm.M = p->M;
+    prm.perms = 1;
+    prm.tie_fix = 0;
+    prm.cw = cw;
+    prm.pm = static_cast<float*>(pm);
+    prm.attempt = att;
+    prm.path = path;
+    prm.att_pm = static_cast<float*>(att_pm);
+    prm.att_cw = att_cw;
+    if (B <= 0) return 0;
+    auto* mp = const_cast<rmfht_plan*>(p);
+    std::call_once(mp->once, [mp] { mp->prepared_rc = mp->prepare(mp); });
+    if (p->prepared_rc != 0) return p->prepared_rc;
+    const long long grid = B < p->grid ? B : p->grid;
+    rmfht2::decode_kernel2<R, MM, L><<<(unsigned)grid, p->nwarps * 32, p->smem, st>>>(prm);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(RMFHT_ECUDA, std::string("decode launch: ") + cudaGetErrorString(e));
+    return 0;
+}
+
+template <int R, int MM, int L>
+int prepare_fast(rmfht_plan* p) {
+    int nw = p->M < 4 ? p->M : 4;
+    if (nw < 1) nw = 1;
+    const size_t smem = rmfht2::smem_bytes2<R, MM, L>(nw);
+    auto kern = rmfht2::decode_kernel2<R, MM, L>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(RMFHT_ECUDA, std::string("smem attribute: ") + cudaGetErrorString(e));
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem);
+    if (e != cudaSuccess || per_sm < 1) return fail(RMFHT_ECUDA, "kernel does not fit an SM");
+    p->nwarps = nw;
+    p->smem = smem;
+    p->grid = sms * per_sm;
+    return 0;
+}
+
+template <typename T, int R, int MM, int L>
+int bind_one(rmfht_plan* p) {
+    if constexpr (sizeof(T) == 4 && (1 << MM) >= 32 && L <= 8) {
+        if (p->fast && p->perms) {
+            p->launch = &launch_fast<R, MM, L>;
+            p->prepare = &prepare_fast<R, MM, L>;
+            return 0;
+        }
+    }
+    p->fast = 0;
+    p->launch = &launch_impl<T, R, MM, L>;
+    p->prepare = &prepare<T, R, MM, L>;
+    return 0;
+}
+
 }  // namespace
 
 int BINDER(RMFHT_T, RMFHT_CHUNK)(rmfht_plan* p) {
 #define X(R_, M_, L_)                                          \
-    if (p->r == R_ && p->m == M_ && p->L == L_) {              \
-        p->launch = &launch_impl<RMFHT_T, R_, M_, L_>;         \
-        p->prepare = &prepare<RMFHT_T, R_, M_, L_>;            \
-        return 0;                                              \
-    }
+    if (p->r == R_ && p->m == M_ && p->L == L_) return bind_one<RMFHT_T, R_, M_, L_>(p);
     CHUNK_MACRO(RMFHT_CHUNK)(X)
 #undef X
     return RMFHT_EUNSUPPORTED;

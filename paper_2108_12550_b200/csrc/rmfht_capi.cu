@@ -138,6 +138,7 @@ int rmfht_plan_create(int r, int m, int L, int M, int flags, int dtype, rmfht_pl
     p->M = p->perms ? M : 1;
     p->dtype = dtype;
     p->tie_fix = dtype == RMFHT_F32 ? 1 : 0;
+    p->fast = (dtype == RMFHT_F32 && !(flags & RMFHT_REFERENCE_ORDER)) ? 1 : 0;
     if (flags & RMFHT_TIE_FIX) p->tie_fix = 1;
     if (flags & RMFHT_NO_TIE_FIX) p->tie_fix = 0;
     if (p->perms) {
@@ -169,6 +170,8 @@ int rmfht_plan_map_sizes(const rmfht_plan* p, int* sizes) {
 int rmfht_plan_record_u16(const rmfht_plan* p) { return p ? 2 * p->m + 2 : fail(RMFHT_EVALUE, "plan is NULL"); }
 
 int rmfht_plan_launches_per_call(const rmfht_plan* p) { return p ? 1 : 0; }
+
+int rmfht_plan_kernel(const rmfht_plan* p) { return p ? (p->fast ? 2 : 1) : 0; }
 
 int rmfht_expand_maps(const rmfht_plan* p, const uint16_t* raw, uint16_t* rec, long long count) {
     if (!p) return fail(RMFHT_EVALUE, "plan is NULL");

@@ -1,0 +1,922 @@
+// B200 (sm_100a) float32 throughput kernel for p-FHT-FSCL-L-M ("v2").
+//
+// Same decoder as rmfht_kernels.cuh (the float64 reference-exact kernel),
+// re-laid out for throughput:
+//   * one warp = one (frame, attempt); the L list paths own 32/L lanes each
+//     ("lane group"); a node vector of size n lives in REGISTERS, element
+//     e = k*LPP + u in register slot k of lane u of its path's group, so f/g
+//     are register-local and an FHT needs log2(LPP) shuffle stages only;
+//   * the channel LLRs of the frame sit in shared memory (root gathers) and
+//     in registers in "channel layout" (lane l holds alpha[l + 32 s]) for the
+//     permutation-extension reliabilities;
+//   * root gathers cost one 3-input XOR and one LDS per element (affine index
+//     tables), no per-element bit loops;
+//   * LM (automorphism.py:232-233) is summed in a canonical channel-domain
+//     order, so trials that pair the same channel entries get bit-identical
+//     LM (the structural ties of SURVEY §8(c) stay exact without a tie fix);
+//   * the FHT top-k / pool step (fht_decode.py:116-120) filters candidates
+//     with an exact path-metric threshold before any sorting.
+// The summation orders are restated by the oracle's float32 mode
+// (oracle/rmo_impl.h, RMO_ORDER_V2), which is how bit-exact parity of this
+// kernel is checked.  FHT butterflies run in the reference's stage order.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "rmfht_kernels.cuh"  // MapS, Params, maps_per_attempt, helpers
+
+namespace rmfht2 {
+
+using rmfht::MapS;
+using rmfht::kFull;
+using u32 = uint32_t;
+using u64 = unsigned long long;
+
+__host__ __device__ constexpr int clog2(int x) { return x <= 1 ? 0 : 1 + clog2(x >> 1); }
+__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// f_op (list_engine.py:15-20): min(|a|,|b|) with the sign of a*b
+// (sgn(0) = +1 only changes the sign of a zero result, which never matters)
+__device__ __forceinline__ float f_op(float a, float b) {
+    const float m = fminf(fabsf(a), fabsf(b));
+    return __int_as_float(__float_as_int(m) | (__float_as_int(a * b) & 0x80000000));
+}
+
+constexpr int kCap = 32;  // FHT candidate list capacity (one per lane)
+
+template <int R, int MM, int L>
+struct Cfg {
+    static constexpr int N = 1 << MM;
+    static constexpr int LPP = 32 / L;
+    static constexpr int LB = clog2(LPP);
+    static constexpr int S = rmfht::maps_per_attempt(R, MM, L);
+    static constexpr int NS = N / 32;  // channel slots per lane
+    static constexpr int SPCMAX = 1 << cmin(R + 1, MM);
+};
+
+template <int SS, int LPP>
+struct Lv {
+    static constexpr int n = 1 << SS;
+    static constexpr bool full = n >= LPP;       // every lane of the group active
+    static constexpr int V = full ? n / LPP : 1;  // register slots per lane
+    static constexpr int act = full ? LPP : n;    // active lanes of the group
+};
+
+// per-warp shared scratch
+template <int R, int MM, int L>
+struct alignas(16) WS2 {
+    using C = Cfg<R, MM, L>;
+    MapS maps[C::S > 0 ? C::S : 1];
+    MapS comp[L];     // composite map of each root path (root perm-ext winners)
+    MapS ctmp[L];
+    MapS bestmap;
+    float pm[L], llrabs[L], pmtmp[2 * L];
+    float lm[2 * L];
+    float ca[kCap], cw[kCap], cpm[kCap];
+    int cb[kCap], cp[kCap], celig[kCap];
+    int sel_src[2 * L], sel_bin[2 * L];
+    float sel_w[2 * L], sel_pm[2 * L];
+    int8_t l0[MM + 1][L], l1[MM + 1][L], l2[MM + 1][L], rootchain[L], ord[2 * L];
+    int16_t nmap[MM + 1][L];
+    // SPC scratch: magnitudes, signs, order of the tau+1 least reliable positions
+    float smag[L * C::SPCMAX];
+    uint8_t ssgn[L * C::SPCMAX];
+    uint16_t sord[L * 16];
+    float vbuf[R >= 3 ? L * C::N : 1];  // inner permutation nodes
+    uint8_t ubits[R >= 3 ? L * C::N : 1];
+    uint32_t bestbits[C::N / 32];  // best codeword of this warp (channel domain)
+    uint32_t scrbits[C::N / 32];   // scratch: a path's bits in the permuted domain
+    float best_pm;
+    int best_att, best_path, next_map, ncand, spc_cnt;
+};
+
+template <int R, int MM, int L>
+struct Ctx2 {
+    using C = Cfg<R, MM, L>;
+    WS2<R, MM, L>& ws;
+    const float* alpha;        // frame LLRs (shared memory)
+    float ach[C::NS];          // channel layout: ach[s] = alpha[lane + 32 s]
+    int lane, p, u;
+};
+
+// ------------------------------------------------------------ helpers ----
+template <int MN>
+__device__ __forceinline__ u32 lin_apply(const u32* cols, u32 x) {
+    u32 v = 0;
+#pragma unroll
+    for (int k = 0; k < MN; k++) v ^= (x >> k & 1u) ? cols[k] : 0u;
+    return v;
+}
+
+// group-local xor reduce / broadcast helpers
+template <int LPP, int ACT>
+__device__ __forceinline__ float group_sum_tree(float v) {
+    // ascending offsets 1, 2, 4 ... (mirrored by the oracle, RMO_ORDER_V2)
+#pragma unroll
+    for (int off = 1; off < ACT; off <<= 1) v = v + __shfl_xor_sync(kFull, v, off);
+    return v;
+}
+template <int ACT>
+__device__ __forceinline__ float group_max(float v) {
+#pragma unroll
+    for (int off = 1; off < ACT; off <<= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, off));
+    return v;
+}
+
+// gather tables of one root path: element k*LPP+u of the permuted vector is
+// alpha[base ^ A[k & 7] ^ B[k >> 3]] (byte offsets)
+template <int MM, int LPP, int V>
+struct RootIdx {
+    static constexpr int NA = V < 8 ? V : 8;
+    static constexpr int NB = V / NA;
+    u32 base, A[NA], B[NB];
+    __device__ __forceinline__ void build(const MapS& mp, int u) {
+        constexpr int LB = clog2(LPP);
+        u32 bse = mp.c;
+#pragma unroll
+        for (int b = 0; b < LB; b++) bse ^= (u >> b & 1) ? mp.icol[b] : 0u;
+        base = bse << 2;
+        A[0] = 0;
+#pragma unroll
+        for (int i = 1; i < NA; i++) {
+            const int b = __ffs(i) - 1;  // lowest set bit: A[i] = A[i & (i-1)] ^ col
+            A[i] = A[i & (i - 1)] ^ (mp.icol[LB + b] << 2);
+        }
+        B[0] = 0;
+#pragma unroll
+        for (int i = 1; i < NB; i++) {
+            const int b = __ffs(i) - 1;
+            B[i] = B[i & (i - 1)] ^ (mp.icol[LB + clog2(NA) + b] << 2);
+        }
+    }
+    __device__ __forceinline__ u32 off(int k) const { return base ^ A[k % NA] ^ B[k / NA]; }
+};
+
+__device__ __forceinline__ float lds_byte(const float* base, u32 byteoff) {
+    return *reinterpret_cast<const float*>(reinterpret_cast<const char*>(base) + byteoff);
+}
+
+// ------------------------------------------- FHT node (RR == 1) ---------
+// fhtl (fht_decode.py:101-126) on all L paths (P == L invariant of
+// p-FHT-FSCL).  x[] is this lane's part of its path's node vector.
+// Writes the survivors (pool order) into ws.sel_*; returns packed bits of
+// this lane group's survivor codeword; lineage into lin[].
+template <int R, int MM, int L, int SS>
+__device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_t* lin) {
+    using C = Cfg<R, MM, L>;
+    using LV = Lv<SS, C::LPP>;
+    constexpr int n = LV::n, V = LV::V, K = cmin(L, n);
+    auto& ws = cx.ws;
+    const int lane = cx.lane, p = cx.p, u = cx.u;
+    const bool act = LV::full || u < n;
+    // llr_abs (:114): lane partial in slot order, then the group tree
+    float part = act ? fabsf(x[0]) : 0.f;
+#pragma unroll
+    for (int k = 1; k < V; k++) part += fabsf(x[k]);
+    const float llrabs = group_sum_tree<C::LPP, LV::act>(part);
+    // butterflies (:28-48): register bits (high) first, then lane bits
+    float w[V];
+#pragma unroll
+    for (int k = 0; k < V; k++) w[k] = act ? x[k] : 0.f;
+#pragma unroll
+    for (int hr = V / 2; hr >= 1; hr >>= 1)
+#pragma unroll
+        for (int k = 0; k < V; k++)
+            if (!(k & hr)) {
+                const float lo = w[k], hi = w[k + hr];
+                w[k] = hi - lo;
+                w[k + hr] = hi + lo;
+            }
+#pragma unroll
+    for (int half = LV::act / 2; half >= 1; half >>= 1) {
+        const float sg = (u & half) ? 1.f : -1.f;
+#pragma unroll
+        for (int k = 0; k < V; k++) {
+            const float o = __shfl_xor_sync(kFull, w[k], half);
+            w[k] = __fmaf_rn(sg, w[k], o);  // hi: w + o = hi + lo; lo: o - w = hi - lo
+        }
+    }
+    // path maximum and the pool threshold tau = L-th smallest path-best pm
+    float mx = act ? fabsf(w[0]) : -1.f;
+#pragma unroll
+    for (int k = 1; k < V; k++) mx = fmaxf(mx, fabsf(w[k]));
+    const float M1 = group_max<LV::act>(mx);
+    const float pmp = ws.pm[p];
+    const float cbest = pmp + 0.5f * (llrabs - M1);
+    float tau = cbest;
+#pragma unroll
+    for (int off = C::LPP; off < 32; off <<= 1) tau = fmaxf(tau, __shfl_xor_sync(kFull, tau, off));
+    // |w| >= theta is implied by pm(|w|) <= tau (with slack for rounding)
+    const float th0 = llrabs - 2.f * (tau - pmp);
+    const float theta = th0 - (fabsf(th0) + llrabs + fabsf(tau) + fabsf(pmp)) * 9.5367431640625e-07f - 1e-30f;
+    u64 mask = 0;
+#pragma unroll
+    for (int k = 0; k < V; k++)
+        if (act && fabsf(w[k]) >= theta) mask |= 1ull << k;
+    // compaction of candidates into the warp list
+    const int cnt = __popcll(mask);
+    int incl = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(kFull, incl, off);
+        if (lane >= off) incl += t;
+    }
+    const int total = __shfl_sync(kFull, incl, 31);
+    bool exact_fallback = total > kCap;
+    if (!exact_fallback) {
+        int pos = incl - cnt;
+        u64 mk = mask;
+        int rounds = cnt;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) rounds = max(rounds, __shfl_xor_sync(kFull, rounds, off));
+        for (int r = 0; r < rounds; r++) {
+            if (mk) {
+                const int k = __ffsll((long long)mk) - 1;
+                mk &= mk - 1;
+                float v = 0.f;
+#pragma unroll
+                for (int kk = 0; kk < V; kk++)
+                    if (kk == k) v = w[kk];
+                ws.ca[pos] = fabsf(v);
+                ws.cw[pos] = v;
+                ws.cb[pos] = LV::full ? k * C::LPP + u : u;
+                ws.cp[pos] = p;
+                pos++;
+            }
+        }
+        {
+            const float la = __shfl_sync(kFull, llrabs, (lane % L) * C::LPP);
+            if (lane < L) ws.llrabs[lane] = la;
+        }
+        __syncwarp();
+        // exact pool over the candidates (fht_decode.py:116-120)
+        int elig = 0, grank = 0;
+        float pmi = 0.f, ai = 0.f;
+        int bi = 0, pi = 0;
+        if (lane < total) {
+            ai = ws.ca[lane];
+            bi = ws.cb[lane];
+            pi = ws.cp[lane];
+            pmi = ws.pm[pi] + 0.5f * (ws.llrabs[pi] - ai);
+            int rp = 0;
+            for (int j = 0; j < total; j++) {
+                const float aj = ws.ca[j];
+                rp += (ws.cp[j] == pi) && (aj > ai || (aj == ai && ws.cb[j] < bi));
+            }
+            elig = rp < K;
+            ws.cpm[lane] = pmi;
+            ws.celig[lane] = elig;
+        }
+        __syncwarp();
+        if (lane < total && elig) {
+            for (int j = 0; j < total; j++) {
+                if (!ws.celig[j]) continue;
+                const float pj = ws.cpm[j];
+                const int sj = ws.cp[j];
+                grank += (pj < pmi) || (pj == pmi && (sj < pi || (sj == pi && ws.cb[j] < bi)));
+            }
+            if (grank < L) {
+                ws.sel_src[grank] = pi;
+                ws.sel_bin[grank] = bi;
+                ws.sel_w[grank] = ws.cw[lane];
+                ws.sel_pm[grank] = pmi;
+            }
+        }
+        __syncwarp();
+    } else {
+        // rare: exact K-round selection per path, then the pool (as rmfht_kernels.cuh)
+        {
+            const float la = __shfl_sync(kFull, llrabs, (lane % L) * C::LPP);
+            if (lane < L) ws.llrabs[lane] = la;
+        }
+        u64 taken = 0ull;
+        for (int rr = 0; rr < K; rr++) {
+            float bv = -1.f, bw = 0.f;
+            int bb = 0x7fffffff;
+#pragma unroll
+            for (int k = 0; k < V; k++) {
+                const int e = LV::full ? k * C::LPP + u : u;
+                const float a = fabsf(w[k]);
+                if (act && !((taken >> k) & 1ull) && (a > bv || (a == bv && e < bb))) { bv = a; bb = e; bw = w[k]; }
+            }
+#pragma unroll
+            for (int off = 1; off < LV::act; off <<= 1) {
+                const float ov = __shfl_xor_sync(kFull, bv, off), ow = __shfl_xor_sync(kFull, bw, off);
+                const int ob = __shfl_xor_sync(kFull, bb, off);
+                if (ov > bv || (ov == bv && ob < bb)) { bv = ov; bb = ob; bw = ow; }
+            }
+            if (act && (LV::full ? (bb % C::LPP) == u : bb == u)) taken |= 1ull << (LV::full ? bb / C::LPP : 0);
+            if (u == 0) {
+                ws.ca[p * K + rr] = bv;
+                ws.cb[p * K + rr] = bb;
+                ws.cw[p * K + rr] = bw;
+                ws.cp[p * K + rr] = p;
+            }
+        }
+        __syncwarp();
+        constexpr int PK = L * K;
+        for (int c = lane; c < PK; c += 32) ws.cpm[c] = ws.pm[c / K] + 0.5f * (ws.llrabs[c / K] - ws.ca[c]);
+        __syncwarp();
+        for (int c = lane; c < PK; c += 32) {
+            const float pc = ws.cpm[c];
+            const int sc = c / K, bc = ws.cb[c];
+            int rank = 0;
+            for (int d = 0; d < PK; d++) {
+                const float pd = ws.cpm[d];
+                const int sd = d / K;
+                rank += (pd < pc) || (pd == pc && (sd < sc || (sd == sc && ws.cb[d] < bc)));
+            }
+            if (rank < L) {
+                ws.sel_src[rank] = sc;
+                ws.sel_bin[rank] = bc;
+                ws.sel_w[rank] = ws.cw[c];
+                ws.sel_pm[rank] = pc;
+            }
+        }
+        __syncwarp();
+    }
+    // survivors: pm, lineage; my group's codeword bits
+    if (lane < L) {
+        ws.pm[lane] = ws.sel_pm[lane];
+        lin[lane] = (int8_t)ws.sel_src[lane];
+    }
+    const int b = ws.sel_bin[p];
+    const int sgn = ws.sel_w[p] < 0.f;
+    __syncwarp();
+    // bit k of the packed word = codeword bit of element k*LPP+u:
+    // parity(~b & ~e & (n-1)) xor sign (_bin_codewords, fht_decode.py:58-62)
+    u64 bits = 0;
+#pragma unroll
+    for (int k = 0; k < V; k++) {
+        const int e = LV::full ? k * C::LPP + u : u;
+        const u64 bit = (u64)((__popc((unsigned)(~(b | e)) & (unsigned)(n - 1)) & 1) ^ sgn);
+        bits |= bit << k;
+    }
+    return act ? bits : 0ull;
+}
+
+// ---------------------------------------------------- SPC node ----------
+// spc_decode_list (list_engine.py:68-119) on L paths of size n = 2^SS.
+template <int R, int MM, int L, int SS>
+__device__ u64 spc_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_t* lin) {
+    using C = Cfg<R, MM, L>;
+    using LV = Lv<SS, C::LPP>;
+    constexpr int n = LV::n, V = LV::V;
+    constexpr int TAU = cmin(cmin(L, n), n - 1);
+    auto& ws = cx.ws;
+    const int lane = cx.lane, p = cx.p, u = cx.u;
+    const bool act = LV::full || u < n;
+    // magnitudes and signs to shared memory, parity by ballot
+    int par = 0;
+#pragma unroll
+    for (int k = 0; k < V; k++) {
+        const int e = LV::full ? k * C::LPP + u : u;
+        if (act) {
+            ws.smag[p * n + e] = fabsf(x[k]);
+            ws.ssgn[p * n + e] = x[k] < 0.f;
+        }
+        const u32 bal = __ballot_sync(kFull, act && x[k] < 0.f);
+        par ^= __popc(bal & (((1u << (LV::act - 1)) << 1) - 1u) << (p * C::LPP)) & 1;
+    }
+    __syncwarp();
+    // rank of each element in the stable ascending |alpha| order (:83); the
+    // TAU+1 least reliable positions go to sord
+#pragma unroll
+    for (int k = 0; k < V; k++) {
+        const int e = LV::full ? k * C::LPP + u : u;
+        if (act) {
+            const float me = ws.smag[p * n + e];
+            int rank = 0;
+            for (int j = 0; j < n; j++) {
+                const float mj = ws.smag[p * n + j];
+                rank += (mj < me) || (mj == me && j < e);
+            }
+            if (rank <= TAU) ws.sord[p * 16 + rank] = (uint16_t)e;
+        }
+    }
+    __syncwarp();
+    // the TAU splits (:97-112): one lane per candidate
+    // path parity for each path (lane group uniform) -> smem
+    if (u == 0) ws.sel_bin[p] = par;
+    __syncwarp();
+    if (lane < L) {
+        const int pp = lane;
+        const float amin = ws.smag[pp * n + ws.sord[pp * 16]];
+        ws.pm[pp] = ws.pm[pp] + (ws.sel_bin[pp] ? amin : 0.f);  // :88
+        ws.sel_w[pp] = (float)ws.sel_bin[pp];                   // running parity
+        ws.sel_src[pp] = pp;                                     // parent path
+        ws.cb[pp] = 0;                                           // flip mask over j
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (int j = 1; j <= TAU; j++) {
+        // candidates: 2i = keep, 2i+1 = flip (interleaved, :101-104)
+        float cand = 0.f;
+        int csrc = 0;
+        if (lane < 2 * L) {
+            const int i = lane >> 1;
+            const int par_i = ws.sel_src[i];
+            const float pmi = ws.pm[i];
+            if (lane & 1) {
+                const float aj = ws.smag[par_i * n + ws.sord[par_i * 16 + j]];
+                const float am = ws.smag[par_i * n + ws.sord[par_i * 16]];
+                const float t = pmi + aj;
+                cand = ws.sel_w[i] != 0.f ? t - am : t + am;
+            } else {
+                cand = pmi;
+            }
+            csrc = i;
+            ws.cpm[lane] = cand;
+        }
+        __syncwarp();
+        int rank = 0;
+        if (lane < 2 * L) {
+            for (int c = 0; c < 2 * L; c++) {
+                const float pc = ws.cpm[c];
+                rank += (pc < cand) || (pc == cand && c < lane);
+            }
+        }
+        // new state (read old state before the sync, write after)
+        float npar = 0.f;
+        int npa = 0, nfl = 0;
+        if (lane < 2 * L && rank < L) {
+            const int which = lane & 1;
+            npar = which ? 1.f - ws.sel_w[csrc] : ws.sel_w[csrc];
+            npa = ws.sel_src[csrc];
+            nfl = ws.cb[csrc] | (which << j);
+        }
+        __syncwarp();
+        if (lane < 2 * L && rank < L) {
+            ws.pm[rank] = cand;
+            ws.sel_w[rank] = npar;
+            ws.sel_src[rank] = npa;
+            ws.cb[rank] = nfl;
+        }
+        __syncwarp();
+    }
+    // beta = sign xor flips, least reliable fixes even parity (:114-118);
+    // my group's output path is slot p
+    const int parent = ws.sel_src[p];
+    const int fl = ws.cb[p];
+    int tot = 0;
+    // parity of sign bits of the parent and of the flips
+    for (int j = 0; j < n; j++) tot ^= ws.ssgn[parent * n + j];
+    tot ^= __popc(fl) & 1;
+    const int least = ws.sord[parent * 16];
+    u64 bits = 0;
+#pragma unroll
+    for (int k = 0; k < V; k++) {
+        const int e = LV::full ? k * C::LPP + u : u;
+        int b = ws.ssgn[parent * n + e];
+        for (int j = 1; j <= TAU; j++)
+            if ((fl >> j & 1) && ws.sord[parent * 16 + j] == e) b ^= 1;
+        if (e == least) b ^= tot;
+        bits |= (u64)b << k;
+    }
+    if (lane < L) lin[lane] = (int8_t)ws.sel_src[lane];
+    __syncwarp();
+    return act ? bits : 0ull;
+}
+
+
+// ------------------------------------------- lane-transposed reduction ----
+// Sum T per-lane partials (one per trial) over the 32 lanes with the tree
+// offsets 16, 8, 4, 2, 1; every trial gets the same tree.  Lane l ends with
+// the total of trial t(l); returns t(l) via *tri.
+template <int T>
+__device__ __forceinline__ float multi_tree(float (&v)[T], int lane, int* tri) {
+    int base = 0;
+    int cnt = T;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        if (cnt > 1) {
+            const int half = cnt / 2;
+            const bool upper = (lane & off) != 0;
+#pragma unroll
+            for (int i = 0; i < T / 2; i++) {
+                if (i < half) {
+                    const float send = upper ? v[i] : v[i + half];
+                    const float keep = upper ? v[i + half] : v[i];
+                    v[i] = keep + __shfl_xor_sync(kFull, send, off);
+                }
+            }
+            if (upper) base += half;
+            cnt = half;
+        } else {
+            v[0] = v[0] + __shfl_xor_sync(kFull, v[0], off);
+        }
+    }
+    *tri = base;
+    return v[0];
+}
+
+// LM partial of one lane for pairing direction d (c = d >> 5 != 0): slots
+// with bit hb of s clear, ascending, partner alpha[(l + 32 s) ^ d]
+template <int NS, int CC>
+__device__ __forceinline__ float lm_case(const float (&ach)[NS], int delta) {
+    constexpr int HB = clog2(CC);  // highest set bit of CC
+    float acc = 0.f;
+    bool first = true;
+#pragma unroll
+    for (int s = 0; s < NS; s++) {
+        if (s >> HB & 1) continue;
+        const float partner = __shfl_xor_sync(kFull, ach[s ^ CC], delta);
+        const float m = fminf(fabsf(ach[s]), fabsf(partner));
+        acc = first ? m : acc + m;
+        first = false;
+    }
+    return acc;
+}
+
+template <int NS, int CC>
+__device__ __forceinline__ float lm_dispatch(const float (&ach)[NS], int c, int delta) {
+    if constexpr (CC >= NS) {
+        return 0.f;
+    } else {
+        if (c == CC) return lm_case<NS, CC>(ach, delta);
+        return lm_dispatch<NS, CC + 1>(ach, c, delta);
+    }
+}
+
+// LM of trial direction d at the root, canonical channel-domain order
+template <int NS>
+__device__ __forceinline__ float lm_partial_root(const float (&ach)[NS], u32 d, int lane) {
+    const int delta = d & 31, c = d >> 5;
+    if (c != 0) return lm_dispatch<NS, 1>(ach, c, delta);
+    // d < 32: pairs inside a slot across lanes l, l ^ d; lanes with bit h clear own them
+    const int h = 31 - __clz(delta);
+    const bool own = !((lane >> h) & 1);
+    float acc = 0.f;
+#pragma unroll
+    for (int s = 0; s < NS; s++) {
+        const float partner = __shfl_xor_sync(kFull, ach[s], delta);
+        const float m = fminf(fabsf(ach[s]), fabsf(partner));
+        acc = (s == 0) ? m : acc + m;
+    }
+    return own ? acc : 0.f;
+}
+
+// top-L of 2L trials by LM descending, lower trial first (automorphism.py:234)
+template <int R, int MM, int L>
+__device__ void select_trials2(Ctx2<R, MM, L>& cx) {
+    auto& ws = cx.ws;
+    const int lane = cx.lane;
+    if (lane < 2 * L) {
+        const float v = ws.lm[lane];
+        int rank = 0;
+#pragma unroll
+        for (int s = 0; s < 2 * L; s++) rank += (ws.lm[s] > v) || (ws.lm[s] == v && s < lane);
+        if (rank < L) ws.ord[rank] = (int8_t)lane;
+    }
+    __syncwarp();
+}
+
+// root permutation extension (automorphism.py:207-237) with the composite
+// maps (init then trial); the winners' composites replace ws.comp
+template <int R, int MM, int L>
+__device__ void perm_ext_root2(Ctx2<R, MM, L>& cx) {
+    using C = Cfg<R, MM, L>;
+    auto& ws = cx.ws;
+    const int lane = cx.lane, base = ws.next_map;
+    // pairing direction of each trial's composite: A_init^-1 (A_t^-1 e_{m-1})
+    if (lane < 2 * L) {
+        const u32 d = lin_apply<MM>(ws.comp[lane % L].icol, ws.maps[base + lane].icol[MM - 1]);
+        ws.cb[lane] = (int)d;
+    }
+    __syncwarp();
+    float part[2 * L];
+#pragma unroll
+    for (int t = 0; t < 2 * L; t++) part[t] = lm_partial_root<C::NS>(cx.ach, (u32)ws.cb[t], lane);
+    int tri;
+    const float tot = multi_tree<2 * L>(part, lane, &tri);
+    if ((lane & (32 / (2 * L) - 1)) == 0) ws.lm[tri] = tot;
+    __syncwarp();
+    select_trials2(cx);
+    // composites of the winners (inverse direction), one column per lane task
+    for (int task = lane; task < L * (MM + 1); task += 32) {
+        const int o = task / (MM + 1), k = task % (MM + 1);
+        const int t = ws.ord[o];
+        const MapS& tm = ws.maps[base + t];
+        const MapS& im = ws.comp[t % L];
+        if (k < MM) ws.ctmp[o].icol[k] = lin_apply<MM>(im.icol, tm.icol[k]);
+        else ws.ctmp[o].c = lin_apply<MM>(im.icol, tm.c) ^ im.c;
+    }
+    float npm = 0.f;
+    if (lane < L) npm = ws.pm[ws.ord[lane] % L];
+    __syncwarp();
+    for (int task = lane; task < L * (MM + 1); task += 32) {
+        const int o = task / (MM + 1), k = task % (MM + 1);
+        if (k < MM) ws.comp[o].icol[k] = ws.ctmp[o].icol[k];
+        else ws.comp[o].c = ws.ctmp[o].c;
+    }
+    if (lane < L) {
+        ws.pm[lane] = npm;
+        ws.l0[MM][lane] = (int8_t)(ws.ord[lane] % L);
+        ws.nmap[MM][lane] = (int16_t)(base + ws.ord[lane]);  // trial map of each root slot
+    }
+    ws.next_map = base + 2 * L;
+    __syncwarp();
+}
+
+// inner permutation node: vectors through shared memory
+template <int R, int MM, int L, int SS>
+__device__ void perm_ext_inner2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V]) {
+    using C = Cfg<R, MM, L>;
+    using LV = Lv<SS, C::LPP>;
+    constexpr int n = LV::n, V = LV::V, H = n / 2;
+    auto& ws = cx.ws;
+    const int lane = cx.lane, p = cx.p, u = cx.u, base = ws.next_map;
+#pragma unroll
+    for (int k = 0; k < V; k++) {
+        const int e = LV::full ? k * C::LPP + u : u;
+        if (LV::full || u < n) ws.vbuf[p * n + e] = x[k];
+    }
+    if (lane < 2 * L) ws.cb[lane] = (int)ws.maps[base + lane].icol[SS - 1];
+    __syncwarp();
+    float part[2 * L];
+#pragma unroll
+    for (int t = 0; t < 2 * L; t++) {
+        const u32 d = (u32)ws.cb[t];
+        const int h = 31 - __clz(d);
+        const int src = t % L;
+        float acc = 0.f;
+        // canonical pairs q = lane + 32 r: i = q with a zero inserted at bit h
+        for (int q = lane, r = 0; q < H; q += 32, r++) {
+            const int i = ((q >> h) << (h + 1)) | (q & ((1 << h) - 1));
+            const float m = fminf(fabsf(ws.vbuf[src * n + i]), fabsf(ws.vbuf[src * n + (i ^ (int)d)]));
+            acc = (r == 0) ? m : acc + m;
+        }
+        part[t] = acc;
+    }
+    int tri;
+    const float tot = multi_tree<2 * L>(part, lane, &tri);
+    if ((lane & (32 / (2 * L) - 1)) == 0) ws.lm[tri] = tot;
+    __syncwarp();
+    select_trials2(cx);
+    // winners: permuted vectors x'[j] = x_src[sigma^-1(j)]
+    const int t = ws.ord[p];
+    const int src = t % L;
+    const MapS& mp = ws.maps[base + t];
+#pragma unroll
+    for (int k = 0; k < V; k++) {
+        const int e = LV::full ? k * C::LPP + u : u;
+        const u32 j = mp.c ^ lin_apply<SS>(mp.icol, (u32)e);
+        x[k] = (LV::full || u < n) ? ws.vbuf[src * n + j] : 0.f;
+    }
+    float npm = 0.f;
+    if (lane < L) npm = ws.pm[ws.ord[lane] % L];
+    __syncwarp();
+    if (lane < L) {
+        ws.pm[lane] = npm;
+        ws.l0[SS][lane] = (int8_t)(ws.ord[lane] % L);
+        ws.nmap[SS][lane] = (int16_t)(base + ws.ord[lane]);
+    }
+    ws.next_map = base + 2 * L;
+    __syncwarp();
+}
+
+// ------------------------------------------------------- tree recursion ----
+template <int R, int MM, int L, int RR, int SS, bool SPINE>
+__device__ u64 node2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_t* lin) {
+    using C = Cfg<R, MM, L>;
+    using LV = Lv<SS, C::LPP>;
+    if constexpr (RR == 1) {
+        return fht_node<R, MM, L, SS>(cx, x, lin);
+    } else if constexpr (RR == SS - 1) {
+        return spc_node<R, MM, L, SS>(cx, x, lin);
+    } else {
+        using LC = Lv<SS - 1, C::LPP>;
+        constexpr int V = LV::V, VC = LC::V, n = LV::n, h = n / 2;
+        constexpr bool INNER_PERM = SPINE && RR >= 2 && SS - RR >= 2 && SS < MM;
+        auto& ws = cx.ws;
+        const int lane = cx.lane, p = cx.p, u = cx.u;
+        int8_t* l0 = ws.l0[SS];
+        int8_t* l1 = ws.l1[SS];
+        int8_t* l2 = ws.l2[SS];
+        if constexpr (INNER_PERM) {
+            perm_ext_inner2<R, MM, L, SS>(cx, x);
+        } else if constexpr (SS < MM) {
+            if (lane < L) l0[lane] = (int8_t)lane;
+            __syncwarp();
+        }
+        // f (:100)
+        float xl[VC];
+        if constexpr (LC::full) {
+#pragma unroll
+            for (int k = 0; k < VC; k++) xl[k] = f_op(x[k], x[k + VC]);
+        } else {
+            const float o = __shfl_down_sync(kFull, x[0], h);
+            xl[0] = (u < h) ? f_op(x[0], o) : 0.f;
+        }
+        const u64 bl = node2<R, MM, L, RR - 1, SS - 1, SPINE>(cx, xl, l1);   // :101
+        // alphas = alphas[lin1] (:102)
+        const int src1 = l1[p];
+        const bool moved = __any_sync(kFull, src1 != p);
+        if (moved) {
+#pragma unroll
+            for (int k = 0; k < V; k++) x[k] = __shfl_sync(kFull, x[k], src1 * C::LPP + u);
+        }
+        // g (:104) with the left child's hard decisions
+        float xr[VC];
+        if constexpr (LC::full) {
+#pragma unroll
+            for (int k = 0; k < VC; k++) {
+                const float sg = ((bl >> k) & 1ull) ? -1.f : 1.f;
+                xr[k] = __fmaf_rn(sg, x[k], x[k + VC]);
+            }
+        } else {
+            const float o = __shfl_down_sync(kFull, x[0], h);
+            const float sg = (bl & 1ull) ? -1.f : 1.f;
+            xr[0] = (u < h) ? __fmaf_rn(sg, x[0], o) : 0.f;
+        }
+        const u64 br = node2<R, MM, L, RR, SS - 1, false>(cx, xr, l2);      // :105
+        // combine (:106-107): beta = [beta_l[lin2] ^ beta_r, beta_r]
+        const int src2 = l2[p];
+        const u64 blm = __shfl_sync(kFull, bl, src2 * C::LPP + u);
+        u64 out;
+        if constexpr (LC::full) {
+            out = (br << VC) | (blm ^ br);
+        } else {
+            const u64 brup = __shfl_up_sync(kFull, br, h);
+            out = (u < h) ? ((blm ^ br) & 1ull) : (brup & 1ull);
+            if (!(LV::full || u < n)) out = 0;
+        }
+        const int chain = l1[src2];
+        if constexpr (INNER_PERM) {
+            // un-permute by this node's trial map (:109-112): out[i] = beta[sigma(i)]
+#pragma unroll
+            for (int k = 0; k < V; k++) {
+                const int e = LV::full ? k * C::LPP + u : u;
+                if (LV::full || u < n) ws.ubits[p * n + e] = (uint8_t)((out >> k) & 1ull);
+            }
+            __syncwarp();
+            const MapS& mp = ws.maps[ws.nmap[SS][chain]];
+            u64 o2 = 0;
+#pragma unroll
+            for (int k = 0; k < V; k++) {
+                const int e = LV::full ? k * C::LPP + u : u;
+                const u32 sidx = mp.b ^ lin_apply<SS>(mp.col, (u32)e);
+                if (LV::full || u < n) o2 |= (u64)ws.ubits[p * n + sidx] << k;
+            }
+            out = o2;
+            __syncwarp();
+        }
+        if (lane < L) {
+            const int ch = l1[l2[lane]];
+            lin[lane] = l0[ch];
+            if (SS == MM) ws.rootchain[lane] = (int8_t)ch;
+        }
+        __syncwarp();
+        return out;
+    }
+}
+
+// ------------------------------------------------------------- kernel ----
+template <int R, int MM, int L>
+__global__ void __launch_bounds__(128) decode_kernel2(rmfht::Params<float> prm) {
+    using C = Cfg<R, MM, L>;
+    using WS = WS2<R, MM, L>;
+    using LV = Lv<MM, C::LPP>;
+    constexpr int N = C::N, S = C::S, NW = N / 32, REC = 2 * MM + 2, V = LV::V;
+    static_assert(N >= 32 && L <= 8, "fast kernel: N >= 32, L <= 8");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* alpha = reinterpret_cast<float*>(smem_raw);
+    WS* wsarr = reinterpret_cast<WS*>(smem_raw + N * sizeof(float));
+    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = lane_id();
+    WS& ws = wsarr[warp];
+    Ctx2<R, MM, L> cx{ws, alpha, {}, lane, lane / C::LPP, lane % C::LPP};
+    constexpr bool ROOT_INTERNAL = !(R == 1 || R == MM - 1);
+
+    for (long long f = blockIdx.x; f < prm.B; f += gridDim.x) {
+        const float4* src4 = reinterpret_cast<const float4*>(prm.llr + f * N);
+        for (int i = threadIdx.x; i < N / 4; i += blockDim.x) reinterpret_cast<float4*>(alpha)[i] = src4[i];
+        __syncthreads();
+#pragma unroll
+        for (int s = 0; s < C::NS; s++) cx.ach[s] = alpha[lane + 32 * s];
+        bool have = false;
+        for (int a = warp; a < prm.M; a += nwarps) {
+            const uint16_t* recs = prm.maps + ((size_t)f * prm.M + a) * S * REC;
+            for (int s = lane; s < S; s += 32) {
+                const int mn = s < L ? MM : MM - (s - L) / (2 * L);
+                rmfht::load_map(ws.maps[s], recs + (size_t)s * REC, MM, mn);
+            }
+            __syncwarp();
+            if (lane < L) {
+                ws.comp[lane] = ws.maps[lane];  // L root maps (:129-139)
+                ws.pm[lane] = 0.f;
+                ws.l0[MM][lane] = (int8_t)lane;
+                ws.nmap[MM][lane] = -1;
+            }
+            ws.next_map = L;
+            __syncwarp();
+            if constexpr (ROOT_INTERNAL) perm_ext_root2(cx);
+            // root gather: x[k] = alpha[sigma_p^-1(k*LPP + u)]
+            float x[V];
+            {
+                RootIdx<MM, C::LPP, V> ri;
+                ri.build(ws.comp[cx.p], cx.u);
+#pragma unroll
+                for (int k = 0; k < V; k++) x[k] = lds_byte(alpha, ri.off(k));
+            }
+            int8_t* rlin = ws.l2[0];  // root lineage (level-0 slot is unused by nodes)
+            const u64 bits = node2<R, MM, L, R, MM, true>(cx, x, rlin);
+            // best path: first minimum (:152)
+            int best = 0;
+#pragma unroll
+            for (int i = 1; i < L; i++)
+                if (ws.pm[i] < ws.pm[best]) best = i;
+            const float pm = ws.pm[best];
+            // root map of the best path: composite slot (perm-ext root) or init map
+            const int rslot = ROOT_INTERNAL ? ws.rootchain[best] : rlin[best];
+            if (prm.att_pm && lane == 0) prm.att_pm[(size_t)f * prm.M + a] = pm;
+            const bool improve = !have || pm < ws.best_pm;  // strict < (:200)
+            if (improve || prm.att_cw) {
+                // packed bits of the best path -> bit array (permuted domain)
+                __syncwarp();
+                uint32_t* bb = ws.scrbits;
+                if (lane < NW) bb[lane] = 0u;
+                __syncwarp();
+                if (cx.p == best) {
+#pragma unroll
+                    for (int k = 0; k < V; k++) {
+                        const int e = k * C::LPP + cx.u;
+                        if ((bits >> k) & 1ull) atomicOr(&bb[e >> 5], 1u << (e & 31));
+                    }
+                }
+                __syncwarp();
+                // forward composite of the best path's root chain: sigma = trial o init
+                if (lane == 0) {
+                    const int init = ROOT_INTERNAL ? ws.l0[MM][rslot] : rslot;
+                    const int trial = ROOT_INTERNAL ? ws.nmap[MM][rslot] : -1;
+                    const MapS& im = ws.maps[init];
+                    if (trial >= 0) {
+                        const MapS& tm = ws.maps[trial];
+#pragma unroll
+                        for (int k = 0; k < MM; k++) ws.ctmp[0].col[k] = lin_apply<MM>(tm.col, im.col[k]);
+                        ws.ctmp[0].b = lin_apply<MM>(tm.col, im.b) ^ tm.b;
+                    } else {
+                        ws.ctmp[0] = im;
+                    }
+                }
+                __syncwarp();
+                // un-permute (:147-150): codeword bit i = beta[sigma(i)]
+                const MapS& fm = ws.ctmp[0];
+                u32 myword = 0;
+#pragma unroll
+                for (int t = 0; t < NW; t++) {
+                    const u32 i = (u32)(t * 32 + lane);
+                    const u32 sidx = fm.b ^ lin_apply<MM>(fm.col, i);
+                    const int bit = (bb[sidx >> 5] >> (sidx & 31)) & 1;
+                    const u32 word = __ballot_sync(kFull, bit);
+                    if (lane == t) myword = word;
+                }
+                if (prm.att_cw && lane < NW) prm.att_cw[((size_t)f * prm.M + a) * NW + lane] = myword;
+                __syncwarp();
+                if (improve) {
+                    if (lane < NW) ws.bestbits[lane] = myword;
+                    if (lane == 0) {
+                        ws.best_pm = pm;
+                        ws.best_att = a;
+                        ws.best_path = best;
+                    }
+                    have = true;
+                }
+                __syncwarp();
+            }
+        }
+        if (!have && lane == 0) ws.best_att = -1;
+        __syncthreads();
+        if (warp == 0) {
+            int bw = -1;
+            if (lane == 0) {
+                for (int w = 0; w < nwarps; w++) {
+                    const WS& o = wsarr[w];
+                    if (o.best_att < 0) continue;
+                    if (bw < 0 || o.best_pm < wsarr[bw].best_pm ||
+                        (o.best_pm == wsarr[bw].best_pm && o.best_att < wsarr[bw].best_att))
+                        bw = w;
+                }
+            }
+            bw = __shfl_sync(kFull, bw, 0);
+            const WS& o = wsarr[bw];
+            if (lane < NW) prm.cw[f * NW + lane] = o.bestbits[lane];
+            if (lane == 0) {
+                prm.pm[f] = o.best_pm;
+                prm.attempt[f] = o.best_att;
+                prm.path[f] = o.best_path;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <int R, int MM, int L>
+constexpr size_t smem_bytes2(int nwarps) {
+    return size_t(1 << MM) * sizeof(float) + sizeof(WS2<R, MM, L>) * size_t(nwarps);
+}
+
+}  // namespace rmfht2

@@ -42,7 +42,7 @@ class Plan:
     """An immutable decode plan bound to a compiled kernel specialisation."""
 
     def __init__(self, r: int, m: int, L: int, M: int = 1, permutations: bool = True,
-                 dtype: str = "f32", tie_fix: bool | None = None):
+                 dtype: str = "f32", tie_fix: bool | None = None, reference_order: bool = False):
         build_code(r, m)
         if L < 1 or M < 1:
             raise ConfigurationError("L, M and P must all be >= 1")
@@ -56,6 +56,8 @@ class Plan:
             flags |= _native.RMFHT_TIE_FIX
         elif tie_fix is False:
             flags |= _native.RMFHT_NO_TIE_FIX
+        if reference_order:
+            flags |= _native.RMFHT_REFERENCE_ORDER
         lib = _native.lib()
         h = ctypes.c_void_p()
         _check(lib.rmfht_plan_create(r, m, L, M, flags,
@@ -70,6 +72,7 @@ class Plan:
         self.rec_u16 = lib.rmfht_plan_record_u16(h)
         self.words = max(1, self.N // 32)
         self.launches_per_call = lib.rmfht_plan_launches_per_call(h)
+        self.kernel = lib.rmfht_plan_kernel(h)  # 1 reference-order, 2 float32 throughput
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -1,7 +1,10 @@
 """CUDA decoder parity (needs a B200).
 
 * float64 kernel vs the reference (golden fixtures): bit-exact on every field.
-* float32 kernel vs the float32 oracle restatement: bit-exact on every field.
+* float32 kernels vs the float32 oracle restatement of the same operation
+  order: bit-exact on every field (the throughput kernel "v2" sums LM and
+  llr_abs in its own order, restated by oracle order="v2"; the
+  reference-order float32 kernel against oracle order="reference").
 * float32 kernel vs the reference: bit-exact on exact-arithmetic fixtures;
   on channel fixtures PM within 1e-5 relative and codewords equal except on
   frames the float64 oracle flags as near-ties (counted, and must be rare).
@@ -15,14 +18,20 @@ NAMES = golden_names()
 pytestmark = pytest.mark.gpu
 
 
-def _plan(g, dtype):
+def _plan(g, dtype, reference_order=False):
     from paper_2108_12550_b200.decoder import Plan
-    return Plan(g["r"], g["m"], g["L"], g["M"], bool(g["perms"]), dtype)
+    return Plan(g["r"], g["m"], g["L"], g["M"], bool(g["perms"]), dtype, reference_order=reference_order)
 
 
-def _gpu(g, dtype):
-    p = _plan(g, dtype)
-    return p.decode(g["llr"], raw_maps=g["raw"] if g["perms"] else None, diag=True)
+def _gpu(g, dtype, reference_order=False):
+    p = _plan(g, dtype, reference_order)
+    out = p.decode(g["llr"], raw_maps=g["raw"] if g["perms"] else None, diag=True)
+    out["kernel"] = p.kernel
+    return out
+
+
+def _order(kernel):
+    return "v2" if kernel == 2 else "reference"
 
 
 @pytest.mark.parametrize("name", NAMES)
@@ -36,12 +45,13 @@ def test_f64_kernel_bit_exact_with_reference(name):
     assert np.array_equal(o["att_cw"], g["att_cw_bits"])
 
 
+@pytest.mark.parametrize("reference_order", [False, True])
 @pytest.mark.parametrize("name", NAMES)
-def test_f32_kernel_bit_exact_with_f32_oracle(name, oracle_mod):
+def test_f32_kernel_bit_exact_with_f32_oracle(name, reference_order, oracle_mod):
     g = load_golden(name)
-    o = _gpu(g, "f32")
+    o = _gpu(g, "f32", reference_order)
     c = oracle_mod.decode(g["r"], g["m"], g["L"], g["M"], g["llr"], g["raw"] if g["perms"] else None,
-                          perms=bool(g["perms"]), dtype=np.float32, nthreads=8)
+                          perms=bool(g["perms"]), dtype=np.float32, nthreads=8, order=_order(o["kernel"]))
     assert np.array_equal(o["cw"], c["cw"])
     assert np.array_equal(o["pm"], c["pm"])
     assert np.array_equal(o["attempt"], c["attempt"])
@@ -70,3 +80,56 @@ def test_f32_kernel_against_reference(name, oracle_mod):
     same = np.all(g["att_cw_bits"][np.arange(len(a)), a] == g["cw_bits"], axis=1)
     near = np.abs(g["att_pm"][np.arange(len(a)), a] - g["pm"]) <= 1e-5 * np.maximum(np.abs(g["pm"]), 1.0)
     assert np.all((same & near) | differ)
+
+
+# ------------------------------------------------ larger batches, headline shapes
+SHAPES = [(2, 9, 4, 20, 2.5, 512), (2, 7, 2, 4, 2.0, 4096), (3, 7, 8, 32, 4.0, 256), (2, 9, 1, 512, 3.0, 48),
+          (2, 9, 4, 20, 1.0, 256)]
+
+
+@pytest.mark.parametrize("r,m,L,M,ebn0,B", SHAPES)
+def test_batch_f32_bit_exact_with_oracle(r, m, L, M, ebn0, B, oracle_mod):
+    from paper_2108_12550_b200.channel_model import synthetic_frames
+    from paper_2108_12550_b200.decoder import Plan
+    from paper_2108_12550_b200.rm_core import build_code, is_codeword
+    spec = build_code(r, m)
+    x, llr = synthetic_frames(spec, ebn0, B, seed=11 + r + m)
+    plan = Plan(r, m, L, M, True, "f32")
+    raw, rec = plan.sample(B, seed=5, identity_root=True)
+    o = plan.decode(llr, records=rec)
+    c = oracle_mod.decode(r, m, L, M, llr, raw, dtype=np.float32, nthreads=16, order=_order(plan.kernel),
+                          want_attempts=False)
+    assert np.array_equal(o["cw"], c["cw"])
+    assert np.array_equal(o["pm"], c["pm"])
+    assert np.array_equal(o["attempt"], c["attempt"])
+    assert np.array_equal(o["path"], c["path"])
+    for f in range(0, B, max(1, B // 16)):
+        assert is_codeword(spec, o["cw"][f])
+
+
+@pytest.mark.parametrize("r,m,L,M,ebn0,B", SHAPES[:3])
+def test_batch_f64_bit_exact_with_oracle(r, m, L, M, ebn0, B, oracle_mod):
+    from paper_2108_12550_b200.channel_model import synthetic_frames
+    from paper_2108_12550_b200.decoder import Plan
+    from paper_2108_12550_b200.rm_core import build_code
+    spec = build_code(r, m)
+    x, llr = synthetic_frames(spec, ebn0, B // 2, seed=3)
+    plan = Plan(r, m, L, M, True, "f64")
+    raw, rec = plan.sample(B // 2, seed=9, identity_root=True)
+    o = plan.decode(llr.astype(np.float64), records=rec)
+    c = oracle_mod.decode(r, m, L, M, llr.astype(np.float64), raw, dtype=np.float64, nthreads=16,
+                          want_attempts=False)
+    assert np.array_equal(o["cw"], c["cw"]) and np.array_equal(o["pm"], c["pm"])
+    assert np.array_equal(o["attempt"], c["attempt"])
+
+
+def test_zero_noise_round_trip():
+    from paper_2108_12550_b200.decoder import Plan
+    from paper_2108_12550_b200.rm_core import build_code, polar_transform, random_message
+    spec = build_code(2, 9)
+    rng = np.random.default_rng(4)
+    x = np.stack([polar_transform(random_message(spec, rng)) for _ in range(64)])
+    plan = Plan(2, 9, 4, 20, True, "f32")
+    _, rec = plan.sample(64, seed=2)
+    o = plan.decode(((1.0 - 2.0 * x) * 4.0).astype(np.float32), records=rec)
+    assert np.array_equal(o["cw"], x) and np.all(o["pm"] == 0)
