@@ -27,8 +27,7 @@ def build() -> str:
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(_LIB_PATH):
-            build()
+        build()  # make: a no-op when up to date, loud when the sources do not compile
         _lib = ctypes.CDLL(_LIB_PATH)
         P = ctypes.c_void_p
         for sfx in ("f64", "f32"):

@@ -92,8 +92,6 @@ static REAL FN(v2_lane_tree)(REAL *v)
     return v[0];
 }
 
-static int rmo_hibit(unsigned x) { return 31 - __builtin_clz(x); }
-
 /* RMO_ORDER_V2 LM at the root: pairs (i, i^d) of channel indices, lane l
  * owning i = l + 32 s (rmfht_fast.cuh, lm_partial_root). */
 static REAL FN(v2_lm_root)(const REAL *alpha, int N, unsigned d)

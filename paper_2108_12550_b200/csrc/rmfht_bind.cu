@@ -89,8 +89,24 @@ int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
     auto* mp = const_cast<rmfht_plan*>(p);
     std::call_once(mp->once, [mp] { mp->prepared_rc = mp->prepare(mp); });
     if (p->prepared_rc != 0) return p->prepared_rc;
-    const long long grid = B < p->grid ? B : p->grid;
-    rmfht2::decode_kernel2<R, MM, L><<<(unsigned)grid, p->nwarps * 32, p->smem, st>>>(prm);
+    const size_t items = (size_t)B * p->M;
+    const size_t need = items * rmfht2::work_bytes2<R, MM, L>();
+    {
+        std::lock_guard<std::mutex> g(mp->work_mu);
+        if (need > mp->work_cap) {
+            if (mp->work) cudaFree(mp->work);
+            mp->work = nullptr;
+            mp->work_cap = 0;
+            if (cudaMalloc(&mp->work, need) != cudaSuccess) return fail(RMFHT_ECUDA, "workspace allocation failed");
+            mp->work_cap = need;
+        }
+    }
+    auto* hdr = static_cast<rmfht2::AttHdr*>(mp->work);
+    auto* bits = reinterpret_cast<unsigned long long*>(static_cast<char*>(mp->work) + items * sizeof(rmfht2::AttHdr));
+    const long long blocks_needed = ((long long)items + p->nwarps - 1) / p->nwarps;
+    const long long grid = blocks_needed < p->grid ? blocks_needed : p->grid;
+    rmfht2::decode_kernel2<R, MM, L><<<(unsigned)grid, p->nwarps * 32, p->smem, st>>>(prm, hdr, bits);
+    rmfht2::reduce_kernel2<R, MM, L><<<(unsigned)((B + 7) / 8), 256, 0, st>>>(prm, hdr, bits);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(RMFHT_ECUDA, std::string("decode launch: ") + cudaGetErrorString(e));
     return 0;
@@ -98,8 +114,7 @@ int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
 
 template <int R, int MM, int L>
 int prepare_fast(rmfht_plan* p) {
-    int nw = p->M < 4 ? p->M : 4;
-    if (nw < 1) nw = 1;
+    int nw = 12;
     const size_t smem = rmfht2::smem_bytes2<R, MM, L>(nw);
     auto kern = rmfht2::decode_kernel2<R, MM, L>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -169,7 +169,7 @@ int rmfht_plan_map_sizes(const rmfht_plan* p, int* sizes) {
 
 int rmfht_plan_record_u16(const rmfht_plan* p) { return p ? 2 * p->m + 2 : fail(RMFHT_EVALUE, "plan is NULL"); }
 
-int rmfht_plan_launches_per_call(const rmfht_plan* p) { return p ? 1 : 0; }
+int rmfht_plan_launches_per_call(const rmfht_plan* p) { return p ? (p->fast ? 2 : 1) : 0; }
 
 int rmfht_plan_kernel(const rmfht_plan* p) { return p ? (p->fast ? 2 : 1) : 0; }
 

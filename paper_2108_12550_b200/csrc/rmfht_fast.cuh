@@ -70,14 +70,17 @@ struct Lv {
 template <int R, int MM, int L>
 struct alignas(16) WS2 {
     using C = Cfg<R, MM, L>;
+    float alpha[C::N];          // this warp's frame LLRs
+    float lmp[2 * L][32];       // LM lane partials per trial
     MapS maps[C::S > 0 ? C::S : 1];
     MapS comp[L];     // composite map of each root path (root perm-ext winners)
     MapS ctmp[L];
     MapS bestmap;
     float pm[L], llrabs[L], pmtmp[2 * L];
     float lm[2 * L];
-    float ca[kCap], cw[kCap], cpm[kCap];
-    int cb[kCap], cp[kCap], celig[kCap];
+    static constexpr int CA = kCap > L * L ? kCap : L * L;  // candidate list (and the exact fallback)
+    float ca[CA], cw[CA], cpm[CA];
+    int cb[CA], cp[CA], celig[CA];
     int sel_src[2 * L], sel_bin[2 * L];
     float sel_w[2 * L], sel_pm[2 * L];
     int8_t l0[MM + 1][L], l1[MM + 1][L], l2[MM + 1][L], rootchain[L], ord[2 * L];
@@ -160,6 +163,71 @@ __device__ __forceinline__ float lds_byte(const float* base, u32 byteoff) {
     return *reinterpret_cast<const float*>(reinterpret_cast<const char*>(base) + byteoff);
 }
 
+// Rare path of fht_node (more candidates than kCap): exact K-round selection
+// per path, then the pool — as the reference-order kernel does it.
+template <int R, int MM, int L, int SS>
+__device__ __noinline__ void fht_fallback(Ctx2<R, MM, L>& cx, const float (&w)[Lv<SS, 32 / L>::V], float llrabs) {
+    using C = Cfg<R, MM, L>;
+    using LV = Lv<SS, C::LPP>;
+    constexpr int n = LV::n, V = LV::V, K = cmin(L, n);
+    auto& ws = cx.ws;
+    const int lane = cx.lane, p = cx.p, u = cx.u;
+    const bool act = LV::full || u < n;
+        // rare: exact K-round selection per path, then the pool (as rmfht_kernels.cuh)
+        {
+            const float la = __shfl_sync(kFull, llrabs, (lane % L) * C::LPP);
+            if (lane < L) ws.llrabs[lane] = la;
+        }
+        u64 taken = 0ull;
+#pragma unroll 1
+        for (int rr = 0; rr < K; rr++) {
+            float bv = -1.f, bw = 0.f;
+            int bb = 0x7fffffff;
+#pragma unroll
+            for (int k = 0; k < V; k++) {
+                const int e = LV::full ? k * C::LPP + u : u;
+                const float a = fabsf(w[k]);
+                if (act && !((taken >> k) & 1ull) && (a > bv || (a == bv && e < bb))) { bv = a; bb = e; bw = w[k]; }
+            }
+#pragma unroll
+            for (int off = 1; off < LV::act; off <<= 1) {
+                const float ov = __shfl_xor_sync(kFull, bv, off), ow = __shfl_xor_sync(kFull, bw, off);
+                const int ob = __shfl_xor_sync(kFull, bb, off);
+                if (ov > bv || (ov == bv && ob < bb)) { bv = ov; bb = ob; bw = ow; }
+            }
+            if (act && (LV::full ? (bb % C::LPP) == u : bb == u)) taken |= 1ull << (LV::full ? bb / C::LPP : 0);
+            if (u == 0) {
+                ws.ca[p * K + rr] = bv;
+                ws.cb[p * K + rr] = bb;
+                ws.cw[p * K + rr] = bw;
+                ws.cp[p * K + rr] = p;
+            }
+        }
+        __syncwarp();
+        constexpr int PK = L * K;
+        for (int c = lane; c < PK; c += 32) ws.cpm[c] = ws.pm[c / K] + 0.5f * (ws.llrabs[c / K] - ws.ca[c]);
+        __syncwarp();
+#pragma unroll 1
+        for (int c = lane; c < PK; c += 32) {
+            const float pc = ws.cpm[c];
+            const int sc = c / K, bc = ws.cb[c];
+            int rank = 0;
+#pragma unroll 1
+            for (int d = 0; d < PK; d++) {
+                const float pd = ws.cpm[d];
+                const int sd = d / K;
+                rank += (pd < pc) || (pd == pc && (sd < sc || (sd == sc && ws.cb[d] < bc)));
+            }
+            if (rank < L) {
+                ws.sel_src[rank] = sc;
+                ws.sel_bin[rank] = bc;
+                ws.sel_w[rank] = ws.cw[c];
+                ws.sel_pm[rank] = pc;
+            }
+        }
+        __syncwarp();
+    }
+
 // ------------------------------------------- FHT node (RR == 1) ---------
 // fhtl (fht_decode.py:101-126) on all L paths (P == L invariant of
 // p-FHT-FSCL).  x[] is this lane's part of its path's node vector.
@@ -233,6 +301,7 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
         int rounds = cnt;
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) rounds = max(rounds, __shfl_xor_sync(kFull, rounds, off));
+#pragma unroll 1
         for (int r = 0; r < rounds; r++) {
             if (mk) {
                 const int k = __ffsll((long long)mk) - 1;
@@ -263,6 +332,7 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
             pi = ws.cp[lane];
             pmi = ws.pm[pi] + 0.5f * (ws.llrabs[pi] - ai);
             int rp = 0;
+#pragma unroll 1
             for (int j = 0; j < total; j++) {
                 const float aj = ws.ca[j];
                 rp += (ws.cp[j] == pi) && (aj > ai || (aj == ai && ws.cb[j] < bi));
@@ -273,6 +343,7 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
         }
         __syncwarp();
         if (lane < total && elig) {
+#pragma unroll 1
             for (int j = 0; j < total; j++) {
                 if (!ws.celig[j]) continue;
                 const float pj = ws.cpm[j];
@@ -288,56 +359,7 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
         }
         __syncwarp();
     } else {
-        // rare: exact K-round selection per path, then the pool (as rmfht_kernels.cuh)
-        {
-            const float la = __shfl_sync(kFull, llrabs, (lane % L) * C::LPP);
-            if (lane < L) ws.llrabs[lane] = la;
-        }
-        u64 taken = 0ull;
-        for (int rr = 0; rr < K; rr++) {
-            float bv = -1.f, bw = 0.f;
-            int bb = 0x7fffffff;
-#pragma unroll
-            for (int k = 0; k < V; k++) {
-                const int e = LV::full ? k * C::LPP + u : u;
-                const float a = fabsf(w[k]);
-                if (act && !((taken >> k) & 1ull) && (a > bv || (a == bv && e < bb))) { bv = a; bb = e; bw = w[k]; }
-            }
-#pragma unroll
-            for (int off = 1; off < LV::act; off <<= 1) {
-                const float ov = __shfl_xor_sync(kFull, bv, off), ow = __shfl_xor_sync(kFull, bw, off);
-                const int ob = __shfl_xor_sync(kFull, bb, off);
-                if (ov > bv || (ov == bv && ob < bb)) { bv = ov; bb = ob; bw = ow; }
-            }
-            if (act && (LV::full ? (bb % C::LPP) == u : bb == u)) taken |= 1ull << (LV::full ? bb / C::LPP : 0);
-            if (u == 0) {
-                ws.ca[p * K + rr] = bv;
-                ws.cb[p * K + rr] = bb;
-                ws.cw[p * K + rr] = bw;
-                ws.cp[p * K + rr] = p;
-            }
-        }
-        __syncwarp();
-        constexpr int PK = L * K;
-        for (int c = lane; c < PK; c += 32) ws.cpm[c] = ws.pm[c / K] + 0.5f * (ws.llrabs[c / K] - ws.ca[c]);
-        __syncwarp();
-        for (int c = lane; c < PK; c += 32) {
-            const float pc = ws.cpm[c];
-            const int sc = c / K, bc = ws.cb[c];
-            int rank = 0;
-            for (int d = 0; d < PK; d++) {
-                const float pd = ws.cpm[d];
-                const int sd = d / K;
-                rank += (pd < pc) || (pd == pc && (sd < sc || (sd == sc && ws.cb[d] < bc)));
-            }
-            if (rank < L) {
-                ws.sel_src[rank] = sc;
-                ws.sel_bin[rank] = bc;
-                ws.sel_w[rank] = ws.cw[c];
-                ws.sel_pm[rank] = pc;
-            }
-        }
-        __syncwarp();
+        fht_fallback<R, MM, L, SS>(cx, w, llrabs);
     }
     // survivors: pm, lineage; my group's codeword bits
     if (lane < L) {
@@ -588,9 +610,12 @@ __device__ void perm_ext_root2(Ctx2<R, MM, L>& cx) {
         ws.cb[lane] = (int)d;
     }
     __syncwarp();
+#pragma unroll 1
+    for (int t = 0; t < 2 * L; t++) ws.lmp[t][lane] = lm_partial_root<C::NS>(cx.ach, (u32)ws.cb[t], lane);
+    __syncwarp();
     float part[2 * L];
 #pragma unroll
-    for (int t = 0; t < 2 * L; t++) part[t] = lm_partial_root<C::NS>(cx.ach, (u32)ws.cb[t], lane);
+    for (int t = 0; t < 2 * L; t++) part[t] = ws.lmp[t][lane];
     int tri;
     const float tot = multi_tree<2 * L>(part, lane, &tri);
     if ((lane & (32 / (2 * L) - 1)) == 0) ws.lm[tri] = tot;
@@ -775,31 +800,93 @@ __device__ u64 node2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_t* 
     }
 }
 
-// ------------------------------------------------------------- kernel ----
+// ------------------------------------------------------------ root node ----
+// Internal root (1 < r < m-1): the root vectors are never held; f (:100) and
+// g (:104) read them straight from the frame LLRs through each path's
+// composite map, g after the left child's lineage (:102) re-selects the maps.
 template <int R, int MM, int L>
-__global__ void __launch_bounds__(128) decode_kernel2(rmfht::Params<float> prm) {
+__device__ u64 root_node(Ctx2<R, MM, L>& cx, int8_t* lin) {
+    using C = Cfg<R, MM, L>;
+    using LV = Lv<MM, C::LPP>;
+    using LC = Lv<MM - 1, C::LPP>;
+    constexpr int VC = LC::V;
+    static_assert(LC::full, "root children span the lane group");
+    auto& ws = cx.ws;
+    const int lane = cx.lane, p = cx.p, u = cx.u;
+    const float* alpha = ws.alpha;
+    int8_t* l0 = ws.l0[MM];
+    int8_t* l1 = ws.l1[MM];
+    int8_t* l2 = ws.l2[MM];
+    float xl[VC];
+    {
+        RootIdx<MM, C::LPP, LV::V> ri;
+        ri.build(ws.comp[p], u);
+#pragma unroll
+        for (int k = 0; k < VC; k++) xl[k] = f_op(lds_byte(alpha, ri.off(k)), lds_byte(alpha, ri.off(k + VC)));
+    }
+    const u64 bl = node2<R, MM, L, R - 1, MM - 1, true>(cx, xl, l1);
+    float xr[VC];
+    {
+        RootIdx<MM, C::LPP, LV::V> ri;
+        ri.build(ws.comp[l1[p]], u);
+#pragma unroll
+        for (int k = 0; k < VC; k++) {
+            const float sg = ((bl >> k) & 1ull) ? -1.f : 1.f;
+            xr[k] = __fmaf_rn(sg, lds_byte(alpha, ri.off(k)), lds_byte(alpha, ri.off(k + VC)));
+        }
+    }
+    const u64 br = node2<R, MM, L, R, MM - 1, false>(cx, xr, l2);
+    const int src2 = l2[p];
+    const u64 blm = __shfl_sync(kFull, bl, src2 * C::LPP + u);
+    const u64 out = (br << VC) | (blm ^ br);
+    if (lane < L) {
+        const int ch = l1[l2[lane]];
+        lin[lane] = l0[ch];
+        ws.rootchain[lane] = (int8_t)ch;
+    }
+    __syncwarp();
+    return out;
+}
+
+// per-attempt record written by decode_kernel2, reduced by reduce_kernel2
+struct AttHdr {
+    float pm;
+    int path, init_map, trial_map;
+};
+
+// ------------------------------------------------------------- kernel ----
+// Work item = (frame, attempt); warps of a CTA take consecutive items in
+// lock-stepped rounds (they run the same code path, so they share the
+// instruction stream).
+template <int R, int MM, int L>
+__global__ void __launch_bounds__(384, 1) decode_kernel2(rmfht::Params<float> prm, AttHdr* hdr, u64* bitsout) {
     using C = Cfg<R, MM, L>;
     using WS = WS2<R, MM, L>;
     using LV = Lv<MM, C::LPP>;
-    constexpr int N = C::N, S = C::S, NW = N / 32, REC = 2 * MM + 2, V = LV::V;
+    constexpr int N = C::N, S = C::S, REC = 2 * MM + 2, V = LV::V;
     static_assert(N >= 32 && L <= 8, "fast kernel: N >= 32, L <= 8");
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float* alpha = reinterpret_cast<float*>(smem_raw);
-    WS* wsarr = reinterpret_cast<WS*>(smem_raw + N * sizeof(float));
+    WS* wsarr = reinterpret_cast<WS*>(smem_raw);
     const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = lane_id();
     WS& ws = wsarr[warp];
-    Ctx2<R, MM, L> cx{ws, alpha, {}, lane, lane / C::LPP, lane % C::LPP};
+    Ctx2<R, MM, L> cx{ws, ws.alpha, {}, lane, lane / C::LPP, lane % C::LPP};
     constexpr bool ROOT_INTERNAL = !(R == 1 || R == MM - 1);
-
-    for (long long f = blockIdx.x; f < prm.B; f += gridDim.x) {
-        const float4* src4 = reinterpret_cast<const float4*>(prm.llr + f * N);
-        for (int i = threadIdx.x; i < N / 4; i += blockDim.x) reinterpret_cast<float4*>(alpha)[i] = src4[i];
-        __syncthreads();
+    const long long items = prm.B * (long long)prm.M;
+    long long cur_f = -1;
+    for (long long base = (long long)blockIdx.x * nwarps; base < items; base += (long long)gridDim.x * nwarps) {
+        const long long item = base + warp;
+        if (item < items) {
+            const long long f = item / prm.M;
+            const int a = (int)(item % prm.M);
+            if (f != cur_f) {
+                const float4* src4 = reinterpret_cast<const float4*>(prm.llr + f * N);
+                for (int i = lane; i < N / 4; i += 32) reinterpret_cast<float4*>(ws.alpha)[i] = src4[i];
+                __syncwarp();
 #pragma unroll
-        for (int s = 0; s < C::NS; s++) cx.ach[s] = alpha[lane + 32 * s];
-        bool have = false;
-        for (int a = warp; a < prm.M; a += nwarps) {
-            const uint16_t* recs = prm.maps + ((size_t)f * prm.M + a) * S * REC;
+                for (int s = 0; s < C::NS; s++) cx.ach[s] = ws.alpha[lane + 32 * s];
+                cur_f = f;
+            }
+            const uint16_t* recs = prm.maps + (size_t)item * S * REC;
             for (int s = lane; s < S; s += 32) {
                 const int mn = s < L ? MM : MM - (s - L) / (2 * L);
                 rmfht::load_map(ws.maps[s], recs + (size_t)s * REC, MM, mn);
@@ -813,110 +900,120 @@ __global__ void __launch_bounds__(128) decode_kernel2(rmfht::Params<float> prm) 
             }
             ws.next_map = L;
             __syncwarp();
+            int8_t* rlin = ws.l2[0];  // root lineage (level-0 slot is unused by nodes)
+            u64 bits;
             if constexpr (ROOT_INTERNAL) perm_ext_root2(cx);
-            // root gather: x[k] = alpha[sigma_p^-1(k*LPP + u)]
-            float x[V];
-            {
+            if constexpr (ROOT_INTERNAL && Lv<MM - 1, C::LPP>::full) {
+                bits = root_node(cx, rlin);
+            } else {
+                float x[V];
                 RootIdx<MM, C::LPP, V> ri;
                 ri.build(ws.comp[cx.p], cx.u);
 #pragma unroll
-                for (int k = 0; k < V; k++) x[k] = lds_byte(alpha, ri.off(k));
+                for (int k = 0; k < V; k++) x[k] = lds_byte(ws.alpha, ri.off(k));
+                bits = node2<R, MM, L, R, MM, true>(cx, x, rlin);
             }
-            int8_t* rlin = ws.l2[0];  // root lineage (level-0 slot is unused by nodes)
-            const u64 bits = node2<R, MM, L, R, MM, true>(cx, x, rlin);
             // best path: first minimum (:152)
             int best = 0;
 #pragma unroll
             for (int i = 1; i < L; i++)
                 if (ws.pm[i] < ws.pm[best]) best = i;
-            const float pm = ws.pm[best];
-            // root map of the best path: composite slot (perm-ext root) or init map
             const int rslot = ROOT_INTERNAL ? ws.rootchain[best] : rlin[best];
-            if (prm.att_pm && lane == 0) prm.att_pm[(size_t)f * prm.M + a] = pm;
-            const bool improve = !have || pm < ws.best_pm;  // strict < (:200)
-            if (improve || prm.att_cw) {
-                // packed bits of the best path -> bit array (permuted domain)
-                __syncwarp();
-                uint32_t* bb = ws.scrbits;
-                if (lane < NW) bb[lane] = 0u;
-                __syncwarp();
-                if (cx.p == best) {
+            if (lane == 0) {
+                AttHdr h;
+                h.pm = ws.pm[best];
+                h.path = best;
+                h.init_map = ROOT_INTERNAL ? ws.l0[MM][rslot] : rslot;
+                h.trial_map = ROOT_INTERNAL ? ws.nmap[MM][rslot] : -1;
+                hdr[item] = h;
+            }
+            if (cx.p == best) bitsout[(size_t)item * C::LPP + cx.u] = bits;
+            __syncwarp();
+        }
+        __syncthreads();  // keep the CTA's warps on the same code path
+    }
+}
+
+// Per frame: first strict minimum over attempts (top_decoders.py:200), then
+// un-permute the winner's root-domain bits by its composite root map
+// (:147-150): codeword bit i = beta[sigma(i)], sigma = trial o init.
+template <int R, int MM, int L>
+__global__ void __launch_bounds__(256) reduce_kernel2(rmfht::Params<float> prm, const AttHdr* hdr, const u64* bitsin) {
+    using C = Cfg<R, MM, L>;
+    constexpr int N = C::N, NW = N / 32, S = C::S, REC = 2 * MM + 2, LPP = C::LPP;
+    __shared__ u64 sbits[8][LPP];
+    __shared__ MapS smap[8];
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    const long long f = (long long)blockIdx.x * 8 + warp;
+    if (f >= prm.B) return;
+    const int M = prm.M;
+    // first minimum over (pm, attempt)
+    float bp = 0.f;
+    int ba = -1;
+    for (int a = lane; a < M; a += 32) {
+        const float v = hdr[f * M + a].pm;
+        if (ba < 0 || v < bp) { bp = v; ba = a; }
+    }
 #pragma unroll
-                    for (int k = 0; k < V; k++) {
-                        const int e = k * C::LPP + cx.u;
-                        if ((bits >> k) & 1ull) atomicOr(&bb[e >> 5], 1u << (e & 31));
-                    }
-                }
-                __syncwarp();
-                // forward composite of the best path's root chain: sigma = trial o init
-                if (lane == 0) {
-                    const int init = ROOT_INTERNAL ? ws.l0[MM][rslot] : rslot;
-                    const int trial = ROOT_INTERNAL ? ws.nmap[MM][rslot] : -1;
-                    const MapS& im = ws.maps[init];
-                    if (trial >= 0) {
-                        const MapS& tm = ws.maps[trial];
+    for (int off = 16; off >= 1; off >>= 1) {
+        const float ov = __shfl_xor_sync(kFull, bp, off);
+        const int oa = __shfl_xor_sync(kFull, ba, off);
+        if (oa >= 0 && (ba < 0 || ov < bp || (ov == bp && oa < ba))) { bp = ov; ba = oa; }
+    }
+    const int a0 = prm.att_pm ? 0 : ba, a1 = prm.att_pm ? M : ba + 1;
+    for (int a = a0; a < a1; a++) {
+        const long long item = f * M + a;
+        const AttHdr h = hdr[item];
+        if (lane < LPP) sbits[warp][lane] = bitsin[(size_t)item * LPP + lane];
+        if (lane == 0) {
+            MapS im, fm;
+            rmfht::load_map(im, prm.maps + ((size_t)item * S + h.init_map) * REC, MM, MM);
+            if (h.trial_map >= 0) {
+                MapS tm;
+                rmfht::load_map(tm, prm.maps + ((size_t)item * S + h.trial_map) * REC, MM, MM);
 #pragma unroll
-                        for (int k = 0; k < MM; k++) ws.ctmp[0].col[k] = lin_apply<MM>(tm.col, im.col[k]);
-                        ws.ctmp[0].b = lin_apply<MM>(tm.col, im.b) ^ tm.b;
-                    } else {
-                        ws.ctmp[0] = im;
-                    }
-                }
-                __syncwarp();
-                // un-permute (:147-150): codeword bit i = beta[sigma(i)]
-                const MapS& fm = ws.ctmp[0];
-                u32 myword = 0;
+                for (int k = 0; k < MM; k++) fm.col[k] = lin_apply<MM>(tm.col, im.col[k]);
+                fm.b = lin_apply<MM>(tm.col, im.b) ^ tm.b;
+            } else {
+                fm = im;
+            }
+            smap[warp] = fm;
+        }
+        __syncwarp();
+        const MapS& fm = smap[warp];
+        u32 myword = 0;
 #pragma unroll
-                for (int t = 0; t < NW; t++) {
-                    const u32 i = (u32)(t * 32 + lane);
-                    const u32 sidx = fm.b ^ lin_apply<MM>(fm.col, i);
-                    const int bit = (bb[sidx >> 5] >> (sidx & 31)) & 1;
-                    const u32 word = __ballot_sync(kFull, bit);
-                    if (lane == t) myword = word;
-                }
-                if (prm.att_cw && lane < NW) prm.att_cw[((size_t)f * prm.M + a) * NW + lane] = myword;
-                __syncwarp();
-                if (improve) {
-                    if (lane < NW) ws.bestbits[lane] = myword;
-                    if (lane == 0) {
-                        ws.best_pm = pm;
-                        ws.best_att = a;
-                        ws.best_path = best;
-                    }
-                    have = true;
-                }
-                __syncwarp();
+        for (int t = 0; t < NW; t++) {
+            const u32 i = (u32)(t * 32 + lane);
+            const u32 e = fm.b ^ lin_apply<MM>(fm.col, i);
+            const int bit = (int)((sbits[warp][e % LPP] >> (e / LPP)) & 1ull);
+            const u32 word = __ballot_sync(kFull, bit);
+            if (lane == t) myword = word;
+        }
+        if (prm.att_pm) {
+            if (lane == 0) prm.att_pm[item] = h.pm;
+            if (prm.att_cw && lane < NW) prm.att_cw[item * NW + lane] = myword;
+        }
+        if (a == ba) {
+            if (lane < NW) prm.cw[f * NW + lane] = myword;
+            if (lane == 0) {
+                prm.pm[f] = h.pm;
+                prm.attempt[f] = ba;
+                prm.path[f] = h.path;
             }
         }
-        if (!have && lane == 0) ws.best_att = -1;
-        __syncthreads();
-        if (warp == 0) {
-            int bw = -1;
-            if (lane == 0) {
-                for (int w = 0; w < nwarps; w++) {
-                    const WS& o = wsarr[w];
-                    if (o.best_att < 0) continue;
-                    if (bw < 0 || o.best_pm < wsarr[bw].best_pm ||
-                        (o.best_pm == wsarr[bw].best_pm && o.best_att < wsarr[bw].best_att))
-                        bw = w;
-                }
-            }
-            bw = __shfl_sync(kFull, bw, 0);
-            const WS& o = wsarr[bw];
-            if (lane < NW) prm.cw[f * NW + lane] = o.bestbits[lane];
-            if (lane == 0) {
-                prm.pm[f] = o.best_pm;
-                prm.attempt[f] = o.best_att;
-                prm.path[f] = o.best_path;
-            }
-        }
-        __syncthreads();
+        __syncwarp();
     }
 }
 
 template <int R, int MM, int L>
 constexpr size_t smem_bytes2(int nwarps) {
-    return size_t(1 << MM) * sizeof(float) + sizeof(WS2<R, MM, L>) * size_t(nwarps);
+    return sizeof(WS2<R, MM, L>) * size_t(nwarps);
+}
+
+template <int R, int MM, int L>
+constexpr size_t work_bytes2() {
+    return sizeof(AttHdr) + sizeof(u64) * size_t(Cfg<R, MM, L>::LPP);
 }
 
 }  // namespace rmfht2

@@ -24,6 +24,13 @@ struct rmfht_plan {
     PrepareFn prepare;  // CUDA-side binding (shared memory, occupancy), once at the first launch
     std::once_flag once;
     int prepared_rc;
+    // device workspace of the throughput kernel (per-attempt records), grown on demand
+    void* work = nullptr;
+    size_t work_cap = 0;
+    std::mutex work_mu;
+    ~rmfht_plan() {
+        if (work) cudaFree(work);
+    }
 };
 
 namespace rmfht_internal {
