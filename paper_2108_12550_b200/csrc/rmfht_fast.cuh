@@ -81,6 +81,11 @@ struct alignas(16) WS2 {
     static constexpr int CA = kCap > L * L ? kCap : L * L;  // candidate list (and the exact fallback)
     float ca[CA], cw[CA], cpm[CA];
     int cb[CA], cp[CA], celig[CA];
+    u64 ckey[kCap];
+    // FHT outputs spilled for candidate extraction: lane-major, padded (conflict-free STS.128)
+    // largest FHT node: RM(1, m-r+1), the first left descendant (the root when r == 1)
+    static constexpr int VMAX = cmax(4, (R == 1 ? C::N : (C::N >> (R - 1))) / C::LPP);
+    float wsp[32][VMAX + 4];
     int sel_src[2 * L], sel_bin[2 * L];
     float sel_w[2 * L], sel_pm[2 * L];
     int8_t l0[MM + 1][L], l1[MM + 1][L], l2[MM + 1][L], rootchain[L], ord[2 * L];
@@ -294,67 +299,74 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
         if (lane >= off) incl += t;
     }
     const int total = __shfl_sync(kFull, incl, 31);
-    bool exact_fallback = total > kCap;
-    if (!exact_fallback) {
+    if (total <= kCap) {
+        // candidates per path (for the per-path top-K rule, fht_decode.py:116)
+        int pcnt = cnt;
+#pragma unroll
+        for (int off = 1; off < LV::act; off <<= 1) pcnt += __shfl_xor_sync(kFull, pcnt, off);
+        const bool over = __any_sync(kFull, pcnt > K);
         int pos = incl - cnt;
+        if constexpr (V > 2) {
+#pragma unroll
+            for (int k = 0; k < V; k += 4)
+                *reinterpret_cast<float4*>(&ws.wsp[lane][k]) = make_float4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+            __syncwarp();
+        }
         u64 mk = mask;
-        int rounds = cnt;
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) rounds = max(rounds, __shfl_xor_sync(kFull, rounds, off));
-#pragma unroll 1
-        for (int r = 0; r < rounds; r++) {
-            if (mk) {
-                const int k = __ffsll((long long)mk) - 1;
-                mk &= mk - 1;
-                float v = 0.f;
-#pragma unroll
-                for (int kk = 0; kk < V; kk++)
-                    if (kk == k) v = w[kk];
-                ws.ca[pos] = fabsf(v);
-                ws.cw[pos] = v;
-                ws.cb[pos] = LV::full ? k * C::LPP + u : u;
-                ws.cp[pos] = p;
-                pos++;
-            }
-        }
-        {
-            const float la = __shfl_sync(kFull, llrabs, (lane % L) * C::LPP);
-            if (lane < L) ws.llrabs[lane] = la;
+        while (mk) {
+            const int k = __ffsll((long long)mk) - 1;
+            mk &= mk - 1;
+            float v;
+            if constexpr (V > 2) v = ws.wsp[lane][k];
+            else if constexpr (V == 2) v = k ? w[1] : w[0];
+            else v = w[0];
+            const float a = fabsf(v);
+            const int bin = LV::full ? k * C::LPP + u : u;
+            const float pmc = pmp + 0.5f * (llrabs - a);  // :119
+            u32 kb = __float_as_uint(pmc);
+            kb ^= (kb >> 31) ? 0xffffffffu : 0x80000000u;  // order-preserving for any sign
+            ws.ckey[pos] = ((u64)kb << 32) | ((u32)p << 16) | (u32)bin;
+            ws.ca[pos] = a;
+            ws.cw[pos] = v;
+            pos++;
         }
         __syncwarp();
-        // exact pool over the candidates (fht_decode.py:116-120)
-        int elig = 0, grank = 0;
-        float pmi = 0.f, ai = 0.f;
-        int bi = 0, pi = 0;
+        if (over) {
+            // a path with more than K candidates: keep only its top-K by
+            // (|w| desc, bin asc); the rest leave the pool
+            u64 kill = 0;
+            if (lane < total) {
+                const u64 ki = ws.ckey[lane];
+                const int pi = (int)((ki >> 16) & 0xffff), bi = (int)(ki & 0xffff);
+                const float ai = ws.ca[lane];
+                int rp = 0;
+#pragma unroll 1
+                for (int j = 0; j < total; j++) {
+                    const u64 kj = ws.ckey[j];
+                    const float aj = ws.ca[j];
+                    rp += ((int)((kj >> 16) & 0xffff) == pi) && (aj > ai || (aj == ai && (int)(kj & 0xffff) < bi));
+                }
+                kill = rp >= K;
+            }
+            __syncwarp();
+            if (kill) ws.ckey[lane] = ~0ull;
+            __syncwarp();
+        }
+        // pool: rank by (pm, source path, bin) (:120)
         if (lane < total) {
-            ai = ws.ca[lane];
-            bi = ws.cb[lane];
-            pi = ws.cp[lane];
-            pmi = ws.pm[pi] + 0.5f * (ws.llrabs[pi] - ai);
-            int rp = 0;
+            const u64 ki = ws.ckey[lane];
+            if (ki != ~0ull) {
+                int rank = 0;
 #pragma unroll 1
-            for (int j = 0; j < total; j++) {
-                const float aj = ws.ca[j];
-                rp += (ws.cp[j] == pi) && (aj > ai || (aj == ai && ws.cb[j] < bi));
-            }
-            elig = rp < K;
-            ws.cpm[lane] = pmi;
-            ws.celig[lane] = elig;
-        }
-        __syncwarp();
-        if (lane < total && elig) {
-#pragma unroll 1
-            for (int j = 0; j < total; j++) {
-                if (!ws.celig[j]) continue;
-                const float pj = ws.cpm[j];
-                const int sj = ws.cp[j];
-                grank += (pj < pmi) || (pj == pmi && (sj < pi || (sj == pi && ws.cb[j] < bi)));
-            }
-            if (grank < L) {
-                ws.sel_src[grank] = pi;
-                ws.sel_bin[grank] = bi;
-                ws.sel_w[grank] = ws.cw[lane];
-                ws.sel_pm[grank] = pmi;
+                for (int j = 0; j < total; j++) rank += ws.ckey[j] < ki;
+                if (rank < L) {
+                    u32 kb = (u32)(ki >> 32);
+                    kb ^= (kb >> 31) ? 0x80000000u : 0xffffffffu;
+                    ws.sel_src[rank] = (int)((ki >> 16) & 0xffff);
+                    ws.sel_bin[rank] = (int)(ki & 0xffff);
+                    ws.sel_w[rank] = ws.cw[lane];
+                    ws.sel_pm[rank] = __uint_as_float(kb);
+                }
             }
         }
         __syncwarp();
@@ -369,14 +381,26 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
     const int b = ws.sel_bin[p];
     const int sgn = ws.sel_w[p] < 0.f;
     __syncwarp();
-    // bit k of the packed word = codeword bit of element k*LPP+u:
-    // parity(~b & ~e & (n-1)) xor sign (_bin_codewords, fht_decode.py:58-62)
-    u64 bits = 0;
-#pragma unroll
-    for (int k = 0; k < V; k++) {
-        const int e = LV::full ? k * C::LPP + u : u;
-        const u64 bit = (u64)((__popc((unsigned)(~(b | e)) & (unsigned)(n - 1)) & 1) ^ sgn);
-        bits |= bit << k;
+    // bit k of the packed word = codeword bit of element e = k*LPP+u
+    // (_bin_codewords, fht_decode.py:58-62): parity(~b & ~e & (n-1)) ^ sign
+    //   = c0 ^ parity(Bh & k),  B = ~b & (n-1), Bh = B >> log2(LPP),
+    //   c0 = sign ^ parity(B) ^ parity(B & u & (LPP-1))
+    u64 bits;
+    if constexpr (LV::full) {
+        const u32 B = (u32)(~b) & (u32)(n - 1);
+        const u32 Bh = B >> C::LB;
+        const int c0 = sgn ^ (__popc(B) & 1) ^ (__popc(B & (u32)u & (u32)(C::LPP - 1)) & 1);
+        constexpr u64 VM = V >= 64 ? ~0ull : ((1ull << V) - 1ull);
+        u64 P = 0;
+        if (Bh & 1u) P ^= 0xAAAAAAAAAAAAAAAAull;
+        if (Bh & 2u) P ^= 0xCCCCCCCCCCCCCCCCull;
+        if (Bh & 4u) P ^= 0xF0F0F0F0F0F0F0F0ull;
+        if (Bh & 8u) P ^= 0xFF00FF00FF00FF00ull;
+        if (Bh & 16u) P ^= 0xFFFF0000FFFF0000ull;
+        if (Bh & 32u) P ^= 0xFFFFFFFF00000000ull;
+        bits = (c0 ? ~P : P) & VM;
+    } else {
+        bits = (u64)((__popc((unsigned)(~(b | u)) & (unsigned)(n - 1)) & 1) ^ sgn);
     }
     return act ? bits : 0ull;
 }

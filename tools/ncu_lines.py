@@ -1,0 +1,52 @@
+"""Dynamic instruction counts per CUDA source line: joins ncu's SASS page
+(instructions executed per PC) with nvdisasm line info of the same cubin.
+usage: ncu_lines.py REPORT OBJ KERNEL_SUBSTR ITEMS [TOP]"""
+import collections, csv, re, subprocess, sys, tempfile, os, glob
+
+rep, obj, ksub, items = sys.argv[1], sys.argv[2], sys.argv[3], float(sys.argv[4])
+top = int(sys.argv[5]) if len(sys.argv) > 5 else 40
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"],
+                     capture_output=True, text=True).stdout
+rows = list(csv.reader(out.splitlines()))
+h = rows[1]
+iA, iS, iE = h.index("Address"), h.index("Source"), h.index("Instructions Executed")
+execs = []
+for r in rows[2:]:
+    if len(r) > iE and r[iA].startswith("0x"):
+        execs.append((int(r[iA], 16), r[iS].strip(), int(r[iE] or 0)))
+base = execs[0][0]
+d = tempfile.mkdtemp()
+subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=d, capture_output=True)
+cub = glob.glob(os.path.join(d, "*.cubin"))[0]
+dis = subprocess.run(["nvdisasm", "--print-line-info", cub], capture_output=True, text=True).stdout
+line_of = {}
+fn, cur = None, None
+for ln in dis.splitlines():
+    m = re.match(r"\s*\.text\.(\S+):", ln)
+    if m:
+        fn = m.group(1)
+        continue
+    m = re.search(r'//## File "([^"]+)", line (\d+)', ln)
+    if m:
+        cur = (os.path.basename(m.group(1)), int(m.group(2)))
+        continue
+    m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(\S.*)", ln)
+    if m and fn and ksub in fn:
+        line_of[int(m.group(1), 16)] = cur
+cnt = collections.Counter()
+miss = 0
+for addr, src, n in execs:
+    key = line_of.get(addr - base)
+    if key is None:
+        miss += n
+        continue
+    cnt[key] += n
+tot = sum(cnt.values()) + miss
+print(f"total per item {tot / items:.0f} (unmapped {miss / items:.0f})")
+srcs = {}
+for (f, l), n in cnt.most_common(top):
+    if f not in srcs:
+        p = [q for q in glob.glob("/root/repo/**/" + f, recursive=True)]
+        srcs[f] = open(p[0]).read().split("\n") if p else []
+    txt = srcs[f][l - 1].strip()[:80] if srcs[f] and l <= len(srcs[f]) else ""
+    print(f"{n / items:7.1f}  {f}:{l}  {txt}")
