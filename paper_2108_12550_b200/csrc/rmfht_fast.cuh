@@ -85,7 +85,7 @@ struct alignas(16) WS2 {
     // FHT outputs spilled for candidate extraction: lane-major, padded (conflict-free STS.128)
     // largest FHT node: RM(1, m-r+1), the first left descendant (the root when r == 1)
     static constexpr int VMAX = cmax(4, (R == 1 ? C::N : (C::N >> (R - 1))) / C::LPP);
-    float wsp[32][VMAX + 4];
+    alignas(16) float wsp[32][VMAX + 4];
     int sel_src[2 * L], sel_bin[2 * L];
     float sel_w[2 * L], sel_pm[2 * L];
     int8_t l0[MM + 1][L], l1[MM + 1][L], l2[MM + 1][L], rootchain[L], ord[2 * L];
