@@ -42,8 +42,9 @@ enum {
     RMFHT_PERMUTATIONS = 1,   /* p-FHT-FSCL (else FHT-FSCL / FHT-FSC, M forced to 1) */
     RMFHT_TIE_FIX = 2,        /* equal pairing directions keep equal LM (default for F32) */
     RMFHT_NO_TIE_FIX = 4,     /* force it off (default for F64) */
-    RMFHT_REFERENCE_ORDER = 8 /* F32: use the reference-operation-order kernel instead of the
-                                 throughput kernel (whose LM / llr_abs summation orders differ) */
+    RMFHT_REFERENCE_ORDER = 8, /* F32: use the reference-operation-order kernel instead of the
+                                  throughput kernel (whose LM / llr_abs summation orders differ) */
+    RMFHT_NO_LOCKSTEP = 16     /* throughput kernel: no CTA barrier between rounds of work items */
 };
 
 enum {

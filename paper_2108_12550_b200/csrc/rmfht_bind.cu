@@ -78,7 +78,7 @@ int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
     prm.B = B;
     prm.M = p->M;
     prm.perms = 1;
-    prm.tie_fix = 0;
+    prm.tie_fix = p->lockstep ? 0x100 : 0;  // (the fast kernel has no tie fix; flag bits reused)
     prm.cw = cw;
     prm.pm = static_cast<float*>(pm);
     prm.attempt = att;
@@ -114,7 +114,8 @@ int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
 
 template <int R, int MM, int L>
 int prepare_fast(rmfht_plan* p) {
-    int nw = 12;
+    int nw = 16;
+    while (nw > 4 && rmfht2::smem_bytes2<R, MM, L>(nw) > 200 * 1024) nw -= 4;
     const size_t smem = rmfht2::smem_bytes2<R, MM, L>(nw);
     auto kern = rmfht2::decode_kernel2<R, MM, L>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -24,6 +24,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "rmfht_kernels.cuh"  // MapS, Params, maps_per_attempt, helpers
 
 namespace rmfht2 {
@@ -47,6 +49,29 @@ __device__ __forceinline__ float f_op(float a, float b) {
 }
 
 constexpr int kCap = 32;  // FHT candidate list capacity (one per lane)
+
+// packed float32x2 (sm_100 FADD2 / FFMA2): one instruction, two lanes of work
+__device__ __forceinline__ u64 pk(float lo, float hi) {
+    u64 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void upk(u64 v, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); }
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+    u64 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+    u64 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+    u64 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
 
 template <int R, int MM, int L>
 struct Cfg {
@@ -81,7 +106,7 @@ struct alignas(16) WS2 {
     static constexpr int CA = kCap > L * L ? kCap : L * L;  // candidate list (and the exact fallback)
     float ca[CA], cw[CA], cpm[CA];
     int cb[CA], cp[CA], celig[CA];
-    u64 ckey[kCap];
+    alignas(16) u64 ckey[kCap];
     // FHT outputs spilled for candidate extraction: lane-major, padded (conflict-free STS.128)
     // largest FHT node: RM(1, m-r+1), the first left descendant (the root when r == 1)
     static constexpr int VMAX = cmax(4, (R == 1 ? C::N : (C::N >> (R - 1))) / C::LPP);
@@ -256,21 +281,39 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
 #pragma unroll
     for (int k = 0; k < V; k++) w[k] = act ? x[k] : 0.f;
 #pragma unroll
-    for (int hr = V / 2; hr >= 1; hr >>= 1)
+    for (int hr = V / 2; hr >= 1; hr >>= 1) {
+        if (hr >= 2) {
+            // two butterflies per instruction: (k, k+1) against (k+hr, k+hr+1)
 #pragma unroll
-        for (int k = 0; k < V; k++)
-            if (!(k & hr)) {
-                const float lo = w[k], hi = w[k + hr];
+            for (int k = 0; k < V; k += 2)
+                if (!(k & hr)) {
+                    const u64 lo = pk(w[k], w[k + 1]), hi = pk(w[k + hr], w[k + hr + 1]);
+                    upk(sub2(hi, lo), w[k], w[k + 1]);
+                    upk(add2(hi, lo), w[k + hr], w[k + hr + 1]);
+                }
+        } else {
+#pragma unroll
+            for (int k = 0; k < V; k += 2) {
+                const float lo = w[k], hi = w[k + 1];
                 w[k] = hi - lo;
-                w[k + hr] = hi + lo;
+                w[k + 1] = hi + lo;
             }
+        }
+    }
 #pragma unroll
     for (int half = LV::act / 2; half >= 1; half >>= 1) {
         const float sg = (u & half) ? 1.f : -1.f;
+        if constexpr (V >= 2) {
+            const u64 sg2 = pk(sg, sg);
 #pragma unroll
-        for (int k = 0; k < V; k++) {
-            const float o = __shfl_xor_sync(kFull, w[k], half);
-            w[k] = __fmaf_rn(sg, w[k], o);  // hi: w + o = hi + lo; lo: o - w = hi - lo
+            for (int k = 0; k < V; k += 2) {
+                const float o0 = __shfl_xor_sync(kFull, w[k], half), o1 = __shfl_xor_sync(kFull, w[k + 1], half);
+                // hi lane: w + o = hi + lo; lo lane: o - w = hi - lo
+                upk(fma2(sg2, pk(w[k], w[k + 1]), pk(o0, o1)), w[k], w[k + 1]);
+            }
+        } else {
+            const float o = __shfl_xor_sync(kFull, w[0], half);
+            w[0] = __fmaf_rn(sg, w[0], o);
         }
     }
     // path maximum and the pool threshold tau = L-th smallest path-best pm
@@ -286,12 +329,14 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
     // |w| >= theta is implied by pm(|w|) <= tau (with slack for rounding)
     const float th0 = llrabs - 2.f * (tau - pmp);
     const float theta = th0 - (fabsf(th0) + llrabs + fabsf(tau) + fabsf(pmp)) * 9.5367431640625e-07f - 1e-30f;
-    u64 mask = 0;
+    using MaskT = typename std::conditional<(V > 32), u64, u32>::type;
+    MaskT mask = 0;
 #pragma unroll
     for (int k = 0; k < V; k++)
-        if (act && fabsf(w[k]) >= theta) mask |= 1ull << k;
+        if (fabsf(w[k]) >= theta) mask |= (MaskT)1 << k;
+    if (!act) mask = 0;
     // compaction of candidates into the warp list
-    const int cnt = __popcll(mask);
+    const int cnt = sizeof(MaskT) == 8 ? __popcll((u64)mask) : __popc((u32)mask);
     int incl = cnt;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -312,9 +357,9 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
                 *reinterpret_cast<float4*>(&ws.wsp[lane][k]) = make_float4(w[k], w[k + 1], w[k + 2], w[k + 3]);
             __syncwarp();
         }
-        u64 mk = mask;
+        MaskT mk = mask;
         while (mk) {
-            const int k = __ffsll((long long)mk) - 1;
+            const int k = sizeof(MaskT) == 8 ? __ffsll((long long)mk) - 1 : __ffs((int)mk) - 1;
             mk &= mk - 1;
             float v;
             if constexpr (V > 2) v = ws.wsp[lane][k];
@@ -330,6 +375,7 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
             ws.cw[pos] = v;
             pos++;
         }
+        if (lane >= total && lane < ((total + 3) & ~3)) ws.ckey[lane] = ~0ull;  // pad to a multiple of 4
         __syncwarp();
         if (over) {
             // a path with more than K candidates: keep only its top-K by
@@ -357,8 +403,13 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
             const u64 ki = ws.ckey[lane];
             if (ki != ~0ull) {
                 int rank = 0;
+                const int tot4 = (total + 3) & ~3;
 #pragma unroll 1
-                for (int j = 0; j < total; j++) rank += ws.ckey[j] < ki;
+                for (int j = 0; j < tot4; j += 4) {
+                    const ulonglong2 k01 = *reinterpret_cast<const ulonglong2*>(&ws.ckey[j]);
+                    const ulonglong2 k23 = *reinterpret_cast<const ulonglong2*>(&ws.ckey[j + 2]);
+                    rank += (k01.x < ki) + (k01.y < ki) + (k23.x < ki) + (k23.y < ki);
+                }
                 if (rank < L) {
                     u32 kb = (u32)(ki >> 32);
                     kb ^= (kb >> 31) ? 0x80000000u : 0xffffffffu;
@@ -578,21 +629,29 @@ __device__ __forceinline__ float lm_case(const float (&ach)[NS], int delta) {
     return acc;
 }
 
-template <int NS, int CC>
+template <int NS>
 __device__ __forceinline__ float lm_dispatch(const float (&ach)[NS], int c, int delta) {
-    if constexpr (CC >= NS) {
-        return 0.f;
-    } else {
-        if (c == CC) return lm_case<NS, CC>(ach, delta);
-        return lm_dispatch<NS, CC + 1>(ach, c, delta);
+    // c is warp-uniform: one indirect branch, no divergence
+    switch (c) {
+#define RMFHT_LM_CASE(CC) \
+    case CC:              \
+        if constexpr (CC < NS) return lm_case<NS, (CC < NS ? CC : 1)>(ach, delta); \
+        break;
+        RMFHT_LM_CASE(1) RMFHT_LM_CASE(2) RMFHT_LM_CASE(3) RMFHT_LM_CASE(4) RMFHT_LM_CASE(5)
+        RMFHT_LM_CASE(6) RMFHT_LM_CASE(7) RMFHT_LM_CASE(8) RMFHT_LM_CASE(9) RMFHT_LM_CASE(10)
+        RMFHT_LM_CASE(11) RMFHT_LM_CASE(12) RMFHT_LM_CASE(13) RMFHT_LM_CASE(14) RMFHT_LM_CASE(15)
+#undef RMFHT_LM_CASE
+        default:
+            break;
     }
+    return 0.f;
 }
 
 // LM of trial direction d at the root, canonical channel-domain order
 template <int NS>
 __device__ __forceinline__ float lm_partial_root(const float (&ach)[NS], u32 d, int lane) {
     const int delta = d & 31, c = d >> 5;
-    if (c != 0) return lm_dispatch<NS, 1>(ach, c, delta);
+    if (c != 0) return lm_dispatch<NS>(ach, c, delta);
     // d < 32: pairs inside a slot across lanes l, l ^ d; lanes with bit h clear own them
     const int h = 31 - __clz(delta);
     const bool own = !((lane >> h) & 1);
@@ -883,12 +942,12 @@ struct AttHdr {
 // lock-stepped rounds (they run the same code path, so they share the
 // instruction stream).
 template <int R, int MM, int L>
-__global__ void __launch_bounds__(384, 1) decode_kernel2(rmfht::Params<float> prm, AttHdr* hdr, u64* bitsout) {
+__global__ void __launch_bounds__(512, 1) decode_kernel2(rmfht::Params<float> prm, AttHdr* hdr, u64* bitsout) {
     using C = Cfg<R, MM, L>;
     using WS = WS2<R, MM, L>;
     using LV = Lv<MM, C::LPP>;
     constexpr int N = C::N, S = C::S, REC = 2 * MM + 2, V = LV::V;
-    static_assert(N >= 32 && L <= 8, "fast kernel: N >= 32, L <= 8");
+    static_assert(N >= 32 && L <= 8 && N <= 512, "fast kernel: 32 <= N <= 512, L <= 8");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WS* wsarr = reinterpret_cast<WS*>(smem_raw);
     const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = lane_id();
@@ -954,7 +1013,7 @@ __global__ void __launch_bounds__(384, 1) decode_kernel2(rmfht::Params<float> pr
             if (cx.p == best) bitsout[(size_t)item * C::LPP + cx.u] = bits;
             __syncwarp();
         }
-        __syncthreads();  // keep the CTA's warps on the same code path
+        if (prm.tie_fix & 0x100) __syncthreads();  // lock-step rounds: warps share the instruction stream
     }
 }
 

@@ -16,6 +16,7 @@ using PrepareFn = int (*)(rmfht_plan*);
 
 struct rmfht_plan {
     int r, m, L, M, perms, tie_fix, dtype;
+    int lockstep = 1;  // throughput kernel: barrier per round of work items (RMFHT_NO_LOCKSTEP clears)
     int fast;  // float32 throughput kernel (rmfht_fast.cuh) instead of the reference-order one
     int S, nwarps, grid;
     size_t smem;

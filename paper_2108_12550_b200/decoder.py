@@ -42,7 +42,8 @@ class Plan:
     """An immutable decode plan bound to a compiled kernel specialisation."""
 
     def __init__(self, r: int, m: int, L: int, M: int = 1, permutations: bool = True,
-                 dtype: str = "f32", tie_fix: bool | None = None, reference_order: bool = False):
+                 dtype: str = "f32", tie_fix: bool | None = None, reference_order: bool = False,
+                 lockstep: bool = True):
         build_code(r, m)
         if L < 1 or M < 1:
             raise ConfigurationError("L, M and P must all be >= 1")
@@ -58,6 +59,8 @@ class Plan:
             flags |= _native.RMFHT_NO_TIE_FIX
         if reference_order:
             flags |= _native.RMFHT_REFERENCE_ORDER
+        if not lockstep:
+            flags |= _native.RMFHT_NO_LOCKSTEP
         lib = _native.lib()
         h = ctypes.c_void_p()
         _check(lib.rmfht_plan_create(r, m, L, M, flags,
