@@ -48,15 +48,14 @@ __device__ __forceinline__ float f_op(float a, float b) {
     return __int_as_float(__float_as_int(m) | (__float_as_int(a * b) & 0x80000000));
 }
 
-constexpr int kCap = 32;  // FHT candidate list capacity (one per lane)
+constexpr int kCap = 64;  // FHT candidate list capacity (two per lane)
 
 // packed float32x2 (sm_100 FADD2 / FFMA2): one instruction, two lanes of work
 __device__ __forceinline__ u64 pk(float lo, float hi) {
-    u64 r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-    return r;
+    return ((u64)__float_as_uint(hi) << 32) | (u64)__float_as_uint(lo);
 }
-__device__ __forceinline__ void upk(u64 v, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); }
+__device__ __forceinline__ float plo(u64 v) { return __uint_as_float((u32)v); }
+__device__ __forceinline__ float phi(u64 v) { return __uint_as_float((u32)(v >> 32)); }
 __device__ __forceinline__ u64 add2(u64 a, u64 b) {
     u64 r;
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -106,7 +105,7 @@ struct alignas(16) WS2 {
     static constexpr int CA = kCap > L * L ? kCap : L * L;  // candidate list (and the exact fallback)
     float ca[CA], cw[CA], cpm[CA];
     int cb[CA], cp[CA], celig[CA];
-    alignas(16) u64 ckey[kCap];
+    alignas(16) u64 ckey[kCap + 4];
     // FHT outputs spilled for candidate extraction: lane-major, padded (conflict-free STS.128)
     // largest FHT node: RM(1, m-r+1), the first left descendant (the root when r == 1)
     static constexpr int VMAX = cmax(4, (R == 1 ? C::N : (C::N >> (R - 1))) / C::LPP);
@@ -196,12 +195,12 @@ __device__ __forceinline__ float lds_byte(const float* base, u32 byteoff) {
 // Rare path of fht_node (more candidates than kCap): exact K-round selection
 // per path, then the pool — as the reference-order kernel does it.
 template <int R, int MM, int L, int SS>
-__device__ __noinline__ void fht_fallback(Ctx2<R, MM, L>& cx, const float (&w)[Lv<SS, 32 / L>::V], float llrabs) {
+__device__ __noinline__ void fht_fallback(WS2<R, MM, L>* wsp_, int lane, float llrabs) {
     using C = Cfg<R, MM, L>;
     using LV = Lv<SS, C::LPP>;
     constexpr int n = LV::n, V = LV::V, K = cmin(L, n);
-    auto& ws = cx.ws;
-    const int lane = cx.lane, p = cx.p, u = cx.u;
+    auto& ws = *wsp_;
+    const int p = lane / C::LPP, u = lane % C::LPP;
     const bool act = LV::full || u < n;
         // rare: exact K-round selection per path, then the pool (as rmfht_kernels.cuh)
         {
@@ -216,8 +215,9 @@ __device__ __noinline__ void fht_fallback(Ctx2<R, MM, L>& cx, const float (&w)[L
 #pragma unroll
             for (int k = 0; k < V; k++) {
                 const int e = LV::full ? k * C::LPP + u : u;
-                const float a = fabsf(w[k]);
-                if (act && !((taken >> k) & 1ull) && (a > bv || (a == bv && e < bb))) { bv = a; bb = e; bw = w[k]; }
+                const float wk = ws.wsp[lane][k];
+                const float a = fabsf(wk);
+                if (act && !((taken >> k) & 1ull) && (a > bv || (a == bv && e < bb))) { bv = a; bb = e; bw = wk; }
             }
 #pragma unroll
             for (int off = 1; off < LV::act; off <<= 1) {
@@ -264,7 +264,7 @@ __device__ __noinline__ void fht_fallback(Ctx2<R, MM, L>& cx, const float (&w)[L
 // Writes the survivors (pool order) into ws.sel_*; returns packed bits of
 // this lane group's survivor codeword; lineage into lin[].
 template <int R, int MM, int L, int SS>
-__device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_t* lin) {
+__device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_t* lin) {
     using C = Cfg<R, MM, L>;
     using LV = Lv<SS, C::LPP>;
     constexpr int n = LV::n, V = LV::V, K = cmin(L, n);
@@ -280,16 +280,21 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
     float w[V];
 #pragma unroll
     for (int k = 0; k < V; k++) w[k] = act ? x[k] : 0.f;
+    constexpr int LOGV = clog2(V);
 #pragma unroll
-    for (int hr = V / 2; hr >= 1; hr >>= 1) {
+    for (int st = 0; st < LOGV; st++) {
+        const int hr = V >> (st + 1);
         if (hr >= 2) {
             // two butterflies per instruction: (k, k+1) against (k+hr, k+hr+1)
 #pragma unroll
             for (int k = 0; k < V; k += 2)
                 if (!(k & hr)) {
                     const u64 lo = pk(w[k], w[k + 1]), hi = pk(w[k + hr], w[k + hr + 1]);
-                    upk(sub2(hi, lo), w[k], w[k + 1]);
-                    upk(add2(hi, lo), w[k + hr], w[k + hr + 1]);
+                    const u64 d = sub2(hi, lo), e = add2(hi, lo);
+                    w[k] = plo(d);
+                    w[k + 1] = phi(d);
+                    w[k + hr] = plo(e);
+                    w[k + hr + 1] = phi(e);
                 }
         } else {
 #pragma unroll
@@ -300,8 +305,10 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
             }
         }
     }
+    constexpr int LOGA = clog2(LV::act);
 #pragma unroll
-    for (int half = LV::act / 2; half >= 1; half >>= 1) {
+    for (int st = 0; st < LOGA; st++) {
+        const int half = LV::act >> (st + 1);
         const float sg = (u & half) ? 1.f : -1.f;
         if constexpr (V >= 2) {
             const u64 sg2 = pk(sg, sg);
@@ -309,7 +316,9 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
             for (int k = 0; k < V; k += 2) {
                 const float o0 = __shfl_xor_sync(kFull, w[k], half), o1 = __shfl_xor_sync(kFull, w[k + 1], half);
                 // hi lane: w + o = hi + lo; lo lane: o - w = hi - lo
-                upk(fma2(sg2, pk(w[k], w[k + 1]), pk(o0, o1)), w[k], w[k + 1]);
+                const u64 r = fma2(sg2, pk(w[k], w[k + 1]), pk(o0, o1));
+                w[k] = plo(r);
+                w[k + 1] = phi(r);
             }
         } else {
             const float o = __shfl_xor_sync(kFull, w[0], half);
@@ -344,6 +353,16 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
         if (lane >= off) incl += t;
     }
     const int total = __shfl_sync(kFull, incl, 31);
+    // spill the transform for candidate extraction (conflict-free STS.128)
+    if constexpr (V >= 4) {
+#pragma unroll
+        for (int k = 0; k < V; k += 4)
+            *reinterpret_cast<float4*>(&ws.wsp[lane][k]) = make_float4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < V; k++) ws.wsp[lane][k] = w[k];
+    }
+    __syncwarp();
     if (total <= kCap) {
         // candidates per path (for the per-path top-K rule, fht_decode.py:116)
         int pcnt = cnt;
@@ -351,20 +370,11 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
         for (int off = 1; off < LV::act; off <<= 1) pcnt += __shfl_xor_sync(kFull, pcnt, off);
         const bool over = __any_sync(kFull, pcnt > K);
         int pos = incl - cnt;
-        if constexpr (V > 2) {
-#pragma unroll
-            for (int k = 0; k < V; k += 4)
-                *reinterpret_cast<float4*>(&ws.wsp[lane][k]) = make_float4(w[k], w[k + 1], w[k + 2], w[k + 3]);
-            __syncwarp();
-        }
         MaskT mk = mask;
         while (mk) {
             const int k = sizeof(MaskT) == 8 ? __ffsll((long long)mk) - 1 : __ffs((int)mk) - 1;
             mk &= mk - 1;
-            float v;
-            if constexpr (V > 2) v = ws.wsp[lane][k];
-            else if constexpr (V == 2) v = k ? w[1] : w[0];
-            else v = w[0];
+            const float v = ws.wsp[lane][k];
             const float a = fabsf(v);
             const int bin = LV::full ? k * C::LPP + u : u;
             const float pmc = pmp + 0.5f * (llrabs - a);  // :119
@@ -375,32 +385,40 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
             ws.cw[pos] = v;
             pos++;
         }
-        if (lane >= total && lane < ((total + 3) & ~3)) ws.ckey[lane] = ~0ull;  // pad to a multiple of 4
+        for (int j = total + lane; j < ((total + 3) & ~3); j += 32) ws.ckey[j] = ~0ull;  // pad to a multiple of 4
         __syncwarp();
         if (over) {
             // a path with more than K candidates: keep only its top-K by
             // (|w| desc, bin asc); the rest leave the pool
-            u64 kill = 0;
-            if (lane < total) {
-                const u64 ki = ws.ckey[lane];
-                const int pi = (int)((ki >> 16) & 0xffff), bi = (int)(ki & 0xffff);
-                const float ai = ws.ca[lane];
-                int rp = 0;
+            bool kill[2] = {false, false};
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int i = lane + 32 * h;
+                if (i < total) {
+                    const u64 ki = ws.ckey[i];
+                    const int pi = (int)((ki >> 16) & 0xffff), bi = (int)(ki & 0xffff);
+                    const float ai = ws.ca[i];
+                    int rp = 0;
 #pragma unroll 1
-                for (int j = 0; j < total; j++) {
-                    const u64 kj = ws.ckey[j];
-                    const float aj = ws.ca[j];
-                    rp += ((int)((kj >> 16) & 0xffff) == pi) && (aj > ai || (aj == ai && (int)(kj & 0xffff) < bi));
+                    for (int j = 0; j < total; j++) {
+                        const u64 kj = ws.ckey[j];
+                        const float aj = ws.ca[j];
+                        rp += ((int)((kj >> 16) & 0xffff) == pi) && (aj > ai || (aj == ai && (int)(kj & 0xffff) < bi));
+                    }
+                    kill[h] = rp >= K;
                 }
-                kill = rp >= K;
             }
             __syncwarp();
-            if (kill) ws.ckey[lane] = ~0ull;
+            if (kill[0]) ws.ckey[lane] = ~0ull;
+            if (kill[1]) ws.ckey[lane + 32] = ~0ull;
             __syncwarp();
         }
         // pool: rank by (pm, source path, bin) (:120)
-        if (lane < total) {
-            const u64 ki = ws.ckey[lane];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int i = lane + 32 * h;
+            if (h == 1 && total <= 32) break;
+            const u64 ki = i < total ? ws.ckey[i] : ~0ull;
             if (ki != ~0ull) {
                 int rank = 0;
                 const int tot4 = (total + 3) & ~3;
@@ -415,14 +433,14 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
                     kb ^= (kb >> 31) ? 0x80000000u : 0xffffffffu;
                     ws.sel_src[rank] = (int)((ki >> 16) & 0xffff);
                     ws.sel_bin[rank] = (int)(ki & 0xffff);
-                    ws.sel_w[rank] = ws.cw[lane];
+                    ws.sel_w[rank] = ws.cw[i];
                     ws.sel_pm[rank] = __uint_as_float(kb);
                 }
             }
         }
         __syncwarp();
     } else {
-        fht_fallback<R, MM, L, SS>(cx, w, llrabs);
+        fht_fallback<R, MM, L, SS>(&cx.ws, lane, llrabs);
     }
     // survivors: pm, lineage; my group's codeword bits
     if (lane < L) {
@@ -459,7 +477,7 @@ __device__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_
 // ---------------------------------------------------- SPC node ----------
 // spc_decode_list (list_engine.py:68-119) on L paths of size n = 2^SS.
 template <int R, int MM, int L, int SS>
-__device__ u64 spc_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_t* lin) {
+__device__ __forceinline__ u64 spc_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_t* lin) {
     using C = Cfg<R, MM, L>;
     using LV = Lv<SS, C::LPP>;
     constexpr int n = LV::n, V = LV::V;
@@ -667,7 +685,7 @@ __device__ __forceinline__ float lm_partial_root(const float (&ach)[NS], u32 d, 
 
 // top-L of 2L trials by LM descending, lower trial first (automorphism.py:234)
 template <int R, int MM, int L>
-__device__ void select_trials2(Ctx2<R, MM, L>& cx) {
+__device__ __forceinline__ void select_trials2(Ctx2<R, MM, L>& cx) {
     auto& ws = cx.ws;
     const int lane = cx.lane;
     if (lane < 2 * L) {
@@ -683,7 +701,7 @@ __device__ void select_trials2(Ctx2<R, MM, L>& cx) {
 // root permutation extension (automorphism.py:207-237) with the composite
 // maps (init then trial); the winners' composites replace ws.comp
 template <int R, int MM, int L>
-__device__ void perm_ext_root2(Ctx2<R, MM, L>& cx) {
+__device__ __forceinline__ void perm_ext_root2(Ctx2<R, MM, L>& cx) {
     using C = Cfg<R, MM, L>;
     auto& ws = cx.ws;
     const int lane = cx.lane, base = ws.next_map;
@@ -732,7 +750,7 @@ __device__ void perm_ext_root2(Ctx2<R, MM, L>& cx) {
 
 // inner permutation node: vectors through shared memory
 template <int R, int MM, int L, int SS>
-__device__ void perm_ext_inner2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V]) {
+__device__ __forceinline__ void perm_ext_inner2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V]) {
     using C = Cfg<R, MM, L>;
     using LV = Lv<SS, C::LPP>;
     constexpr int n = LV::n, V = LV::V, H = n / 2;
@@ -789,7 +807,7 @@ __device__ void perm_ext_inner2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V
 
 // ------------------------------------------------------- tree recursion ----
 template <int R, int MM, int L, int RR, int SS, bool SPINE>
-__device__ u64 node2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_t* lin) {
+__device__ __forceinline__ u64 node2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_t* lin) {
     using C = Cfg<R, MM, L>;
     using LV = Lv<SS, C::LPP>;
     if constexpr (RR == 1) {
@@ -888,7 +906,7 @@ __device__ u64 node2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_t* 
 // g (:104) read them straight from the frame LLRs through each path's
 // composite map, g after the left child's lineage (:102) re-selects the maps.
 template <int R, int MM, int L>
-__device__ u64 root_node(Ctx2<R, MM, L>& cx, int8_t* lin) {
+__device__ __forceinline__ u64 root_node(Ctx2<R, MM, L>& cx, int8_t* lin) {
     using C = Cfg<R, MM, L>;
     using LV = Lv<MM, C::LPP>;
     using LC = Lv<MM - 1, C::LPP>;
