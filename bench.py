@@ -187,7 +187,7 @@ def run_gpu(args):
     from paper_2108_12550_b200.rm_core import build_code
 
     spec = build_code(R, M_VARS)
-    plan = Plan(R, M_VARS, L, M, True, "f32", lockstep=not args.no_lockstep)
+    plan = Plan(R, M_VARS, L, M, True, "f32", lockstep=0 if args.no_lockstep else args.lockstep)
     B = args.frames
     x, llr, recs = make_inputs(plan, spec, B, seed=1 + rank)
     dev = torch.device("cuda", local)
@@ -303,7 +303,8 @@ def main():
     ap.add_argument("--frames", type=int, default=16384)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-lockstep", action="store_true", help="throughput kernel without per-round CTA barriers")
+    ap.add_argument("--no-lockstep", action="store_true", help="throughput kernel without per-round barriers")
+    ap.add_argument("--lockstep", type=int, default=16, choices=[4, 8, 16], help="warps per lock-step group")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
     if args.warmup < 3:

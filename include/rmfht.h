@@ -44,7 +44,9 @@ enum {
     RMFHT_NO_TIE_FIX = 4,     /* force it off (default for F64) */
     RMFHT_REFERENCE_ORDER = 8, /* F32: use the reference-operation-order kernel instead of the
                                   throughput kernel (whose LM / llr_abs summation orders differ) */
-    RMFHT_NO_LOCKSTEP = 16     /* throughput kernel: no CTA barrier between rounds of work items */
+    RMFHT_NO_LOCKSTEP = 16,    /* throughput kernel: no barrier between rounds of work items */
+    RMFHT_LOCKSTEP_4 = 32,     /* ... barrier per group of 4 warps instead of the whole CTA */
+    RMFHT_LOCKSTEP_8 = 64      /* ... per group of 8 warps */
 };
 
 enum {

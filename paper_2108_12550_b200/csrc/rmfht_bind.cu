@@ -78,7 +78,7 @@ int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
     prm.B = B;
     prm.M = p->M;
     prm.perms = 1;
-    prm.tie_fix = p->lockstep ? 0x100 : 0;  // (the fast kernel has no tie fix; flag bits reused)
+    prm.tie_fix = (p->lockstep & 0xff) << 8;  // warps per lock-step group (the fast kernel has no tie fix)
     prm.cw = cw;
     prm.pm = static_cast<float*>(pm);
     prm.attempt = att;

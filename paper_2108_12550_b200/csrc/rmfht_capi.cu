@@ -139,7 +139,9 @@ int rmfht_plan_create(int r, int m, int L, int M, int flags, int dtype, rmfht_pl
     p->dtype = dtype;
     p->tie_fix = dtype == RMFHT_F32 ? 1 : 0;
     p->fast = (dtype == RMFHT_F32 && !(flags & RMFHT_REFERENCE_ORDER)) ? 1 : 0;
-    p->lockstep = (flags & RMFHT_NO_LOCKSTEP) ? 0 : 1;
+    p->lockstep = (flags & RMFHT_NO_LOCKSTEP) ? 0 : 16;
+    if (flags & RMFHT_LOCKSTEP_4) p->lockstep = 4;
+    if (flags & RMFHT_LOCKSTEP_8) p->lockstep = 8;
     if (flags & RMFHT_TIE_FIX) p->tie_fix = 1;
     if (flags & RMFHT_NO_TIE_FIX) p->tie_fix = 0;
     if (p->perms) {

@@ -370,6 +370,12 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
         for (int off = 1; off < LV::act; off <<= 1) pcnt += __shfl_xor_sync(kFull, pcnt, off);
         const bool over = __any_sync(kFull, pcnt > K);
         int pos = incl - cnt;
+        // this path's candidates occupy [pstart, pstart + pcnt) (lane order)
+        const int pstart = __shfl_sync(kFull, incl - cnt, p * C::LPP);
+        if (u == 0) {
+            ws.cp[p] = pstart;
+            ws.celig[p] = pcnt;
+        }
         MaskT mk = mask;
         while (mk) {
             const int k = sizeof(MaskT) == 8 ? __ffsll((long long)mk) - 1 : __ffs((int)mk) - 1;
@@ -385,7 +391,7 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
             ws.cw[pos] = v;
             pos++;
         }
-        for (int j = total + lane; j < ((total + 3) & ~3); j += 32) ws.ckey[j] = ~0ull;  // pad to a multiple of 4
+        if (lane < 4 && total + lane < ((total + 3) & ~3)) ws.ckey[total + lane] = ~0ull;  // pad to 4
         __syncwarp();
         if (over) {
             // a path with more than K candidates: keep only its top-K by
@@ -397,15 +403,17 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
                 if (i < total) {
                     const u64 ki = ws.ckey[i];
                     const int pi = (int)((ki >> 16) & 0xffff), bi = (int)(ki & 0xffff);
-                    const float ai = ws.ca[i];
-                    int rp = 0;
+                    const int j0 = ws.cp[pi], j1 = j0 + ws.celig[pi];
+                    if (j1 - j0 > K) {
+                        const float ai = ws.ca[i];
+                        int rp = 0;
 #pragma unroll 1
-                    for (int j = 0; j < total; j++) {
-                        const u64 kj = ws.ckey[j];
-                        const float aj = ws.ca[j];
-                        rp += ((int)((kj >> 16) & 0xffff) == pi) && (aj > ai || (aj == ai && (int)(kj & 0xffff) < bi));
+                        for (int j = j0; j < j1; j++) {
+                            const float aj = ws.ca[j];
+                            rp += aj > ai || (aj == ai && (int)(ws.ckey[j] & 0xffff) < bi);
+                        }
+                        kill[h] = rp >= K;
                     }
-                    kill[h] = rp >= K;
                 }
             }
             __syncwarp();
@@ -1031,7 +1039,13 @@ __global__ void __launch_bounds__(512, 1) decode_kernel2(rmfht::Params<float> pr
             if (cx.p == best) bitsout[(size_t)item * C::LPP + cx.u] = bits;
             __syncwarp();
         }
-        if (prm.tie_fix & 0x100) __syncthreads();  // lock-step rounds: warps share the instruction stream
+        // lock-step rounds: warps share the instruction stream (named barrier per group)
+        const int grp = (prm.tie_fix >> 8) & 0xff;  // warps per lock-step group, 0 = none
+        if (grp >= nwarps) {
+            __syncthreads();
+        } else if (grp > 0) {
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + warp / grp), "r"(grp * 32) : "memory");
+        }
     }
 }
 

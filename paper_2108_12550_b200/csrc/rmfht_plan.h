@@ -16,7 +16,7 @@ using PrepareFn = int (*)(rmfht_plan*);
 
 struct rmfht_plan {
     int r, m, L, M, perms, tie_fix, dtype;
-    int lockstep = 1;  // throughput kernel: barrier per round of work items (RMFHT_NO_LOCKSTEP clears)
+    int lockstep = 16;  // throughput kernel: warps per lock-step group (0 = none)
     int fast;  // float32 throughput kernel (rmfht_fast.cuh) instead of the reference-order one
     int S, nwarps, grid;
     size_t smem;

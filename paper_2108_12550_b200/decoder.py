@@ -43,7 +43,7 @@ class Plan:
 
     def __init__(self, r: int, m: int, L: int, M: int = 1, permutations: bool = True,
                  dtype: str = "f32", tie_fix: bool | None = None, reference_order: bool = False,
-                 lockstep: bool = True):
+                 lockstep: int = 16):
         build_code(r, m)
         if L < 1 or M < 1:
             raise ConfigurationError("L, M and P must all be >= 1")
@@ -61,6 +61,10 @@ class Plan:
             flags |= _native.RMFHT_REFERENCE_ORDER
         if not lockstep:
             flags |= _native.RMFHT_NO_LOCKSTEP
+        elif lockstep == 4:
+            flags |= _native.RMFHT_LOCKSTEP_4
+        elif lockstep == 8:
+            flags |= _native.RMFHT_LOCKSTEP_8
         lib = _native.lib()
         h = ctypes.c_void_p()
         _check(lib.rmfht_plan_create(r, m, L, M, flags,
