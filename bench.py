@@ -189,7 +189,7 @@ def run_gpu(args):
     spec = build_code(R, M_VARS)
     plan = Plan(R, M_VARS, L, M, True, "f32", lockstep=0 if args.no_lockstep else args.lockstep)
     B = args.frames
-    x, llr, recs = make_inputs(plan, spec, B, seed=1 + rank)
+    x, llr, recs = make_inputs(plan, spec, B, seed=1 + rank)  # host table: decode-only timing
     dev = torch.device("cuda", local)
     d_llr = torch.from_numpy(llr).to(dev)
     d_rec = torch.from_numpy(recs.view(np.int16)).to(dev)
@@ -201,8 +201,15 @@ def run_gpu(args):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
+    SEED = 1 + rank
+
+    def step():
+        # one pass of the hot path: draw the batch's permutations on the device
+        # (the reference samples them inside decode) and decode
+        plan.launch_sampled(d_llr, SEED, out, frame0=0, stream=stream)
+
     for _ in range(args.warmup):
-        plan.launch(d_llr, d_rec, out, stream)
+        step()
     barrier()
     # correctness spot check of the warm-up output (not timed)
     cw = out["cw"].cpu().numpy().view(np.uint32)
@@ -215,7 +222,7 @@ def run_gpu(args):
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
-            plan.launch(d_llr, d_rec, out, stream)
+            step()
         ev1.record(stream)
         barrier()
     ms = ev0.elapsed_time(ev1)
@@ -225,9 +232,20 @@ def run_gpu(args):
     ms = float(t.item())
     value = ws * B * args.steps / (ms / 1e3)
 
-    # e2e through the public path with host buffers, every step
+    # decode only, permutation table resident in HBM (explains value)
+    for _ in range(2):
+        plan.launch(d_llr, d_rec, out, stream)
+    barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        plan.launch(d_llr, d_rec, out, stream)
+    ev1.record(stream)
+    barrier()
+    ms_dec = ev0.elapsed_time(ev1)
+
+    # e2e through the public path with host buffers, every step: pinned host
+    # LLRs in, codewords / PM / attempt out; permutations drawn on the device
     h_llr = torch.from_numpy(llr).pin_memory()
-    h_rec = torch.from_numpy(recs.view(np.int16)).pin_memory()
     h_cw = torch.empty(out["cw"].shape, dtype=torch.int32).pin_memory()
     h_pm = torch.empty(out["pm"].shape, dtype=torch.float32).pin_memory()
     h_att = torch.empty(out["attempt"].shape, dtype=torch.int32).pin_memory()
@@ -235,8 +253,7 @@ def run_gpu(args):
 
     def e2e_step():
         d_llr.copy_(h_llr, non_blocking=True)
-        d_rec.copy_(h_rec, non_blocking=True)
-        plan.launch(d_llr, d_rec, out, stream)
+        plan.launch_sampled(d_llr, SEED, out, frame0=0, stream=stream)
         h_cw.copy_(out["cw"], non_blocking=True)
         h_pm.copy_(out["pm"], non_blocking=True)
         h_att.copy_(out["attempt"], non_blocking=True)
@@ -254,7 +271,7 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_e = float(t.item())
     e2e = ws * B * e_steps / (ms_e / 1e3)
-    h2d = llr.nbytes + recs.nbytes
+    h2d = llr.nbytes
     d2h = h_cw.numel() * 4 + h_pm.numel() * 4 + h_att.numel() * 4
 
     if rank == 0:
@@ -265,7 +282,7 @@ def run_gpu(args):
         per_gpu = value / ws
         ach_gops = ops * per_gpu / 1e9
         bytes_frame = 4 * spec.N + spec.N // 8
-        rec_bytes_frame = M * plan.S * plan.rec_u16 * 2
+        rec_bytes_frame = 2 * M * plan.S * plan.rec_u16 * 2  # table written by the sampler, read by the decoder
         clk = clk.summary()
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
@@ -276,7 +293,9 @@ def run_gpu(args):
                        "fer_check": fer_warm},
             "e2e": {"value": e2e, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps": e_steps},
-            "gpu_launches": args.steps * plan.launches_per_call,
+            "gpu_launches": args.steps * (plan.launches_per_call + 1),
+            "decode_only": {"value": ws * B * args.steps / (ms_dec / 1e3), "ms_per_step": ms_dec / args.steps,
+                            "note": "same batch, permutation table already resident in HBM"},
             "roofline": {"bound": "fp32", "achieved": ach_gops, "peak": peak_gops, "unit": "Gop/s",
                          "frac": ach_gops / peak_gops, "traffic": None,
                          "ops_per_frame": ops,

@@ -87,6 +87,20 @@ int rmfht_expand_maps(const rmfht_plan *plan, const uint16_t *raw, uint16_t *rec
 int rmfht_sample_maps(const rmfht_plan *plan, uint64_t seed, long long frame0, long long B,
                       int identity_root, uint16_t *raw, uint16_t *rec);
 
+/* Device: the same table as rmfht_sample_maps (bit-identical), written as
+ * device records straight to d_rec [B, M, S, 2m+2]; stream-ordered. */
+int rmfht_sample_maps_device(const rmfht_plan *plan, uint64_t seed, long long frame0, long long B,
+                             int identity_root, uint16_t *d_rec, void *stream);
+
+/* Decode B frames whose permutations are drawn on the device from
+ * (seed, frame0 + frame index) — no host table ("NULL for
+ * on-device sampling with (seed, frame_offset)").  The table lives in a
+ * plan-owned device buffer; concurrent calls on one plan must be
+ * stream-serialised. */
+int rmfht_decode_launch_sampled(const rmfht_plan *plan, const void *d_llr, uint64_t seed, long long frame0,
+                                int identity_root, uint32_t *d_cw, void *d_pm, int32_t *d_attempt,
+                                int32_t *d_path, long long B, void *stream);
+
 /* Decode B frames.  d_llr [B, 2^m] float or double (per dtype); d_maps
  * [B, M, S, 2m+2] records (ignored without RMFHT_PERMUTATIONS); outputs
  * d_cw [B, max(1, 2^m/32)] bit-packed codewords (bit i%32 of word i/32),

@@ -29,6 +29,7 @@ EXPORTS = [
     "rmfht_plan_map_sizes", "rmfht_plan_record_u16", "rmfht_expand_maps",
     "rmfht_decode_launch", "rmfht_decode_launch_diag", "rmfht_plan_launches_per_call",
     "rmfht_last_error", "rmfht_version", "rmfht_sample_maps", "rmfht_plan_kernel",
+    "rmfht_sample_maps_device", "rmfht_decode_launch_sampled",
 ]
 
 _lib = None
@@ -99,6 +100,10 @@ def lib():
     L.rmfht_decode_launch_diag.restype = I
     L.rmfht_sample_maps.argtypes = [P, ctypes.c_uint64, LL, LL, I, P, P]
     L.rmfht_sample_maps.restype = I
+    L.rmfht_sample_maps_device.argtypes = [P, ctypes.c_uint64, LL, LL, I, P, P]
+    L.rmfht_sample_maps_device.restype = I
+    L.rmfht_decode_launch_sampled.argtypes = [P, P, ctypes.c_uint64, LL, I, P, P, P, P, LL, P]
+    L.rmfht_decode_launch_sampled.restype = I
     L.rmfht_last_error.argtypes = []
     L.rmfht_last_error.restype = ctypes.c_char_p
     L.rmfht_version.argtypes = []

@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "rmfht_maps.cuh"
 #include "rmfht_plan.h"
 
 namespace rmfht_internal {
@@ -36,85 +37,31 @@ int bind_any(rmfht_plan* p) {
     return fail(RMFHT_EUNSUPPORTED, buf);
 }
 
-// raw (row masks, b) -> record (columns, b, inverse columns, A^-1 b)
-int expand_one(const uint16_t* raw, int mn, int mg, uint16_t* rec) {
-    unsigned rows[16], inv[16];
-    for (int r = 0; r < mn; r++) {
-        rows[r] = raw[r];
-        inv[r] = 1u << r;
-        if (raw[r] >> mn) return -1;
+using rmfht_maps::expand_one;
+
+struct SampleArgs {
+    unsigned long long seed;
+    long long frame0, B;
+    int M, S, L, m, identity_root;
+    signed char sizes[128];
+};
+
+// one thread per (frame, attempt, slot): the same draw as rmfht_sample_maps
+__global__ void sample_kernel(SampleArgs a, uint16_t* rec) {
+    const long long total = a.B * (long long)a.M * a.S;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long f = a.frame0 + i / ((long long)a.M * a.S);
+        const int at = (int)((i / a.S) % a.M), sl = (int)(i % a.S);
+        uint16_t raw[16];
+        rmfht_maps::table_entry(a.seed, f, at, sl, a.L, a.sizes[sl], a.m, a.identity_root, raw);
+        uint16_t r[32];
+        rmfht_maps::expand_one(raw, a.sizes[sl], a.m, r);
+        uint16_t* o = rec + i * (2 * a.m + 2);
+        for (int k = 0; k < 2 * a.m + 2; k++) o[k] = r[k];
     }
-    for (int r = mn; r < mg; r++)
-        if (raw[r]) return -1;
-    const unsigned b = raw[mg];
-    if (b >> mn) return -1;
-    for (int c = 0; c < mn; c++) {  // Gauss-Jordan over GF(2)
-        int piv = -1;
-        for (int r = c; r < mn; r++)
-            if (rows[r] >> c & 1u) { piv = r; break; }
-        if (piv < 0) return -1;
-        std::swap(rows[c], rows[piv]);
-        std::swap(inv[c], inv[piv]);
-        for (int r = 0; r < mn; r++)
-            if (r != c && (rows[r] >> c & 1u)) { rows[r] ^= rows[c]; inv[r] ^= inv[c]; }
-    }
-    std::memset(rec, 0, sizeof(uint16_t) * (2 * mg + 2));
-    unsigned cinv = 0;
-    for (int k = 0; k < mn; k++) {
-        unsigned col = 0, icol = 0;
-        for (int r = 0; r < mn; r++) {
-            col |= (unsigned)((raw[r] >> k) & 1u) << r;
-            icol |= ((inv[r] >> k) & 1u) << r;
-        }
-        rec[k] = (uint16_t)col;
-        rec[mg + 1 + k] = (uint16_t)icol;
-        if (b >> k & 1u) cinv ^= icol;
-    }
-    rec[mg] = (uint16_t)b;
-    rec[2 * mg + 1] = (uint16_t)cinv;
-    return 0;
 }
 
-
-// counter-based generator: one independent stream per (seed, frame, attempt, slot)
-inline uint64_t splitmix64(uint64_t& x) {
-    uint64_t z = (x += 0x9E3779B97F4A7C15ull);
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
-}
-
-// uniform (A, b) in GL(mn,2) x F_2^mn by rejection on random row masks
-// (the reference's rule, automorphism.py:127-161), written as a raw record
-void sample_raw(uint64_t key, int mn, int mg, uint16_t* raw) {
-    uint64_t st = key;
-    const unsigned mask = (1u << mn) - 1u;
-    for (;;) {
-        unsigned rows[16];
-        uint64_t w = 0;
-        for (int r = 0; r < mn; r++) {
-            if (r % 4 == 0) w = splitmix64(st);
-            rows[r] = (unsigned)(w >> (16 * (r % 4))) & mask;
-        }
-        unsigned t[16];
-        for (int r = 0; r < mn; r++) t[r] = rows[r];
-        bool ok = true;
-        for (int c = 0; c < mn && ok; c++) {
-            int piv = -1;
-            for (int r = c; r < mn; r++)
-                if (t[r] >> c & 1u) { piv = r; break; }
-            if (piv < 0) { ok = false; break; }
-            std::swap(t[c], t[piv]);
-            for (int r = c + 1; r < mn; r++)
-                if (t[r] >> c & 1u) t[r] ^= t[c];
-        }
-        if (!ok) continue;
-        for (int k = 0; k <= mg; k++) raw[k] = 0;
-        for (int r = 0; r < mn; r++) raw[r] = (uint16_t)rows[r];
-        raw[mg] = (uint16_t)(splitmix64(st) & mask);
-        return;
-    }
-}
 }  // namespace
 
 extern "C" {
@@ -172,7 +119,7 @@ int rmfht_plan_map_sizes(const rmfht_plan* p, int* sizes) {
 
 int rmfht_plan_record_u16(const rmfht_plan* p) { return p ? 2 * p->m + 2 : fail(RMFHT_EVALUE, "plan is NULL"); }
 
-int rmfht_plan_launches_per_call(const rmfht_plan* p) { return p ? (p->fast ? 2 : 1) : 0; }
+int rmfht_plan_launches_per_call(const rmfht_plan* p) { return p ? (p->fast ? 2 : 1) : 0; }  // + 1 when sampled
 
 int rmfht_plan_kernel(const rmfht_plan* p) { return p ? (p->fast ? 2 : 1) : 0; }
 
@@ -206,19 +153,61 @@ int rmfht_sample_maps(const rmfht_plan* p, uint64_t seed, long long frame0, long
         const int a = (int)((i / S) % M), s = (int)(i % S);
         uint16_t tmp[16], rtmp[32];
         uint16_t* r = raw ? raw + i * (mg + 1) : tmp;
-        if (identity_root && a == 0 && s < p->L) {
-            for (int k = 0; k < mg; k++) r[k] = (uint16_t)(1u << k);
-            r[mg] = 0;
-        } else {
-            uint64_t key = seed * 0xD1B54A32D192ED03ull ^ ((uint64_t)f * 0x9E3779B97F4A7C15ull);
-            uint64_t st = key + ((uint64_t)a << 20) + (uint64_t)s;
-            const uint64_t k2 = splitmix64(st);
-            sample_raw(k2, p->sizes[s], mg, r);
-        }
-        if (rec && expand_one(r, p->sizes[s], mg, rec ? rec + i * (2 * mg + 2) : rtmp) != 0) err |= 1;
+        rmfht_maps::table_entry(seed, f, a, s, p->L, p->sizes[s], mg, identity_root, r);
+        if (rec && expand_one(r, p->sizes[s], mg, rec + i * (2 * mg + 2)) != 0) err |= 1;
+        (void)rtmp;
     }
     if (err) return fail(RMFHT_EVALUE, "internal: sampled a singular map");
     return 0;
+}
+
+int rmfht_sample_maps_device(const rmfht_plan* p, uint64_t seed, long long frame0, long long B, int identity_root,
+                             uint16_t* d_rec, void* stream) {
+    if (!p) return fail(RMFHT_EVALUE, "plan is NULL");
+    if (B < 0 || !d_rec) return fail(RMFHT_EVALUE, "bad arguments");
+    if (p->S > 128) return fail(RMFHT_EUNSUPPORTED, "more than 128 maps per attempt");
+    if (B == 0 || p->S == 0) return 0;
+    SampleArgs a;
+    a.seed = seed;
+    a.frame0 = frame0;
+    a.B = B;
+    a.M = p->M;
+    a.S = p->S;
+    a.L = p->L;
+    a.m = p->m;
+    a.identity_root = identity_root;
+    for (int s = 0; s < p->S; s++) a.sizes[s] = (signed char)p->sizes[s];
+    const long long total = B * (long long)p->M * p->S;
+    long long blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    sample_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, d_rec);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(RMFHT_ECUDA, std::string("sample launch: ") + cudaGetErrorString(e));
+    return 0;
+}
+
+int rmfht_decode_launch_sampled(const rmfht_plan* p, const void* d_llr, uint64_t seed, long long frame0,
+                                int identity_root, uint32_t* d_cw, void* d_pm, int32_t* d_attempt, int32_t* d_path,
+                                long long B, void* stream) {
+    if (!p) return fail(RMFHT_EVALUE, "plan is NULL");
+    if (!p->perms) return rmfht_decode_launch(p, d_llr, nullptr, d_cw, d_pm, d_attempt, d_path, B, stream);
+    auto* mp = const_cast<rmfht_plan*>(p);
+    const size_t need = (size_t)B * p->M * p->S * (2 * p->m + 2) * sizeof(uint16_t);
+    uint16_t* rec;
+    {
+        std::lock_guard<std::mutex> g(mp->work_mu);
+        if (need > mp->maps_cap) {
+            if (mp->maps_buf) cudaFree(mp->maps_buf);
+            mp->maps_buf = nullptr;
+            mp->maps_cap = 0;
+            if (cudaMalloc(&mp->maps_buf, need) != cudaSuccess) return fail(RMFHT_ECUDA, "map table allocation failed");
+            mp->maps_cap = need;
+        }
+        rec = static_cast<uint16_t*>(mp->maps_buf);
+    }
+    int rc = rmfht_sample_maps_device(p, seed, frame0, B, identity_root, rec, stream);
+    if (rc) return rc;
+    return rmfht_decode_launch(p, d_llr, rec, d_cw, d_pm, d_attempt, d_path, B, stream);
 }
 
 int rmfht_decode_launch_diag(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint32_t* cw, void* pm,

@@ -28,9 +28,12 @@ struct rmfht_plan {
     // device workspace of the throughput kernel (per-attempt records), grown on demand
     void* work = nullptr;
     size_t work_cap = 0;
+    void* maps_buf = nullptr;  // device map table of rmfht_decode_launch_sampled
+    size_t maps_cap = 0;
     std::mutex work_mu;
     ~rmfht_plan() {
         if (work) cudaFree(work);
+        if (maps_buf) cudaFree(maps_buf);
     }
 };
 

@@ -118,6 +118,24 @@ class Plan:
             None if rec is None else rec.ctypes.data_as(ctypes.c_void_p)))
         return raw, rec
 
+    def sample_device(self, B: int, seed: int, frame0: int = 0, identity_root: bool = True, stream=None):
+        """Device map records drawn on the GPU (bit-identical to ``sample``)."""
+        torch = _torch()
+        rec = torch.empty((B, self.M, self.S, self.rec_u16), dtype=torch.int16, device="cuda")
+        st = stream if stream is not None else torch.cuda.current_stream()
+        _check(self._lib.rmfht_sample_maps_device(self._h, ctypes.c_uint64(seed), frame0, B, int(identity_root),
+                                                  rec.data_ptr(), st.cuda_stream))
+        return rec
+
+    def launch_sampled(self, llr, seed: int, out: dict, frame0: int = 0, identity_root: bool = True,
+                       stream=None) -> None:
+        """Stream-ordered decode with on-device permutation sampling."""
+        torch = _torch()
+        st = stream if stream is not None else torch.cuda.current_stream()
+        _check(self._lib.rmfht_decode_launch_sampled(
+            self._h, llr.data_ptr(), ctypes.c_uint64(seed), frame0, int(identity_root), out["cw"].data_ptr(),
+            out["pm"].data_ptr(), out["attempt"].data_ptr(), out["path"].data_ptr(), llr.shape[0], st.cuda_stream))
+
     # ---------------------------------------------------------- launch ----
     def alloc_outputs(self, B: int, device=None, diag: bool = False):
         torch = _torch()

@@ -133,3 +133,33 @@ def test_zero_noise_round_trip():
     _, rec = plan.sample(64, seed=2)
     o = plan.decode(((1.0 - 2.0 * x) * 4.0).astype(np.float32), records=rec)
     assert np.array_equal(o["cw"], x) and np.all(o["pm"] == 0)
+
+
+@pytest.mark.parametrize("r,m,L,M", [(2, 9, 4, 20), (3, 7, 8, 32), (2, 7, 2, 4)])
+def test_device_sampler_matches_host(r, m, L, M):
+    import torch
+    from paper_2108_12550_b200.decoder import Plan
+    plan = Plan(r, m, L, M, True, "f32")
+    raw, rec = plan.sample(37, seed=123, frame0=1000, identity_root=True)
+    d = plan.sample_device(37, seed=123, frame0=1000, identity_root=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy().view(np.uint16), rec)
+
+
+def test_sampled_decode_matches_table_decode():
+    import torch
+    from paper_2108_12550_b200.channel_model import synthetic_frames
+    from paper_2108_12550_b200.decoder import Plan
+    from paper_2108_12550_b200.rm_core import build_code
+    spec = build_code(2, 9)
+    _, llr = synthetic_frames(spec, 2.5, 300, seed=8)
+    plan = Plan(2, 9, 4, 20, True, "f32")
+    _, rec = plan.sample(300, seed=77, frame0=5)
+    a = plan.decode(llr, records=rec)
+    d_llr = torch.from_numpy(llr).cuda()
+    out = plan.alloc_outputs(300)
+    plan.launch_sampled(d_llr, 77, out, frame0=5)
+    torch.cuda.synchronize()
+    assert np.array_equal(out["cw"].cpu().numpy().view(np.uint32), a["cw_packed"])
+    assert np.array_equal(out["pm"].cpu().numpy(), a["pm"])
+    assert np.array_equal(out["attempt"].cpu().numpy(), a["attempt"])
