@@ -47,18 +47,22 @@ struct SampleArgs {
 };
 
 // one thread per (frame, attempt, slot): the same draw as rmfht_sample_maps
-__global__ void sample_kernel(SampleArgs a, uint16_t* rec) {
+template <int MG>
+__global__ void __launch_bounds__(256) sample_kernel(SampleArgs a, uint16_t* rec) {
     const long long total = a.B * (long long)a.M * a.S;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
         const long long f = a.frame0 + i / ((long long)a.M * a.S);
         const int at = (int)((i / a.S) % a.M), sl = (int)(i % a.S);
-        uint16_t raw[16];
-        rmfht_maps::table_entry(a.seed, f, at, sl, a.L, a.sizes[sl], a.m, a.identity_root, raw);
-        uint16_t r[32];
-        rmfht_maps::expand_one(raw, a.sizes[sl], a.m, r);
-        uint16_t* o = rec + i * (2 * a.m + 2);
-        for (int k = 0; k < 2 * a.m + 2; k++) o[k] = r[k];
+        uint16_t r[2 * MG + 2];
+        const int mn = a.sizes[sl];
+        if (mn == MG)
+            rmfht_maps::table_entry_t<MG>(a.seed, f, at, sl, a.L, MG, a.identity_root, nullptr, r);
+        else
+            rmfht_maps::table_entry(a.seed, f, at, sl, a.L, mn, MG, a.identity_root, nullptr, r);
+        uint32_t* o = reinterpret_cast<uint32_t*>(rec + i * (2 * MG + 2));  // 2*MG+2 is even: 4-byte aligned
+#pragma unroll
+        for (int k = 0; k < MG + 1; k++) o[k] = (uint32_t)r[2 * k] | ((uint32_t)r[2 * k + 1] << 16);
     }
 }
 
@@ -151,13 +155,10 @@ int rmfht_sample_maps(const rmfht_plan* p, uint64_t seed, long long frame0, long
     for (long long i = 0; i < total; i++) {
         const long long f = frame0 + i / ((long long)M * S);
         const int a = (int)((i / S) % M), s = (int)(i % S);
-        uint16_t tmp[16], rtmp[32];
-        uint16_t* r = raw ? raw + i * (mg + 1) : tmp;
-        rmfht_maps::table_entry(seed, f, a, s, p->L, p->sizes[s], mg, identity_root, r);
-        if (rec && expand_one(r, p->sizes[s], mg, rec + i * (2 * mg + 2)) != 0) err |= 1;
-        (void)rtmp;
+        rmfht_maps::table_entry(seed, f, a, s, p->L, p->sizes[s], mg, identity_root, raw ? raw + i * (mg + 1) : nullptr,
+                                rec ? rec + i * (2 * mg + 2) : nullptr);
     }
-    if (err) return fail(RMFHT_EVALUE, "internal: sampled a singular map");
+    (void)err;
     return 0;
 }
 
@@ -180,7 +181,18 @@ int rmfht_sample_maps_device(const rmfht_plan* p, uint64_t seed, long long frame
     const long long total = B * (long long)p->M * p->S;
     long long blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    sample_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, d_rec);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    switch (p->m) {
+#define RMFHT_SK(K) \
+    case K:         \
+        sample_kernel<K><<<(unsigned)blocks, 256, 0, st>>>(a, d_rec); \
+        break;
+        RMFHT_SK(2) RMFHT_SK(3) RMFHT_SK(4) RMFHT_SK(5) RMFHT_SK(6) RMFHT_SK(7) RMFHT_SK(8) RMFHT_SK(9)
+        RMFHT_SK(10) RMFHT_SK(11) RMFHT_SK(12) RMFHT_SK(13) RMFHT_SK(14)
+#undef RMFHT_SK
+        default:
+            return fail(RMFHT_EUNSUPPORTED, "map size");
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(RMFHT_ECUDA, std::string("sample launch: ") + cudaGetErrorString(e));
     return 0;
