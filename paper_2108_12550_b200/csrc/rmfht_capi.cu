@@ -46,23 +46,53 @@ struct SampleArgs {
     signed char sizes[128];
 };
 
-// one thread per (frame, attempt, slot): the same draw as rmfht_sample_maps
+// one warp per (frame, attempt): the classes of its slots are filled with
+// candidates tested 32 at a time (ballot keeps the candidate order)
+template <int MN>
+__device__ __forceinline__ void fill_class_dev(const SampleArgs& a, long long f, int at, int c, int s0, int cnt,
+                                               uint16_t* rec_item) {
+    const int lane = threadIdx.x & 31;
+    int filled = 0;
+    for (long long base = 0; filled < cnt; base += 32) {
+        unsigned rows[MN], inv[MN], b;
+        const bool ok = rmfht_maps::candidate<MN>(rmfht_maps::cand_key(a.seed, f, at, c, base + lane), rows, inv, b);
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        const int rank = __popc(bal & ((1u << lane) - 1u));
+        if (ok && filled + rank < cnt) {
+            uint16_t r[2 * 14 + 2];
+            rmfht_maps::write_map<MN>(rows, inv, b, a.m, nullptr, r);
+            uint16_t* o = rec_item + (size_t)(s0 + filled + rank) * (2 * a.m + 2);
+            for (int k = 0; k < 2 * a.m + 2; k++) o[k] = r[k];
+        }
+        filled += __popc(bal);
+    }
+}
+
 template <int MG>
 __global__ void __launch_bounds__(256) sample_kernel(SampleArgs a, uint16_t* rec) {
-    const long long total = a.B * (long long)a.M * a.S;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long f = a.frame0 + i / ((long long)a.M * a.S);
-        const int at = (int)((i / a.S) % a.M), sl = (int)(i % a.S);
-        uint16_t r[2 * MG + 2];
-        const int mn = a.sizes[sl];
-        if (mn == MG)
-            rmfht_maps::table_entry_t<MG>(a.seed, f, at, sl, a.L, MG, a.identity_root, nullptr, r);
-        else
-            rmfht_maps::table_entry(a.seed, f, at, sl, a.L, mn, MG, a.identity_root, nullptr, r);
-        uint32_t* o = reinterpret_cast<uint32_t*>(rec + i * (2 * MG + 2));  // 2*MG+2 is even: 4-byte aligned
-#pragma unroll
-        for (int k = 0; k < MG + 1; k++) o[k] = (uint32_t)r[2 * k] | ((uint32_t)r[2 * k + 1] << 16);
+    const long long items = a.B * (long long)a.M;
+    const int lane = threadIdx.x & 31;
+    for (long long item = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; item < items;
+         item += (long long)gridDim.x * blockDim.x / 32) {
+        const long long f = a.frame0 + item / a.M;
+        const int at = (int)(item % a.M);
+        uint16_t* rec_item = rec + (size_t)item * a.S * (2 * MG + 2);
+        int s = 0, c = 0;
+        while (s < a.S) {
+            const int mn = a.sizes[s];
+            int e = s;
+            while (e < a.S && a.sizes[e] == mn) e++;
+            int s0 = s;
+            if (a.identity_root && at == 0 && s == 0) {
+                for (int t = lane; t < a.L; t += 32) rmfht_maps::write_identity(mn, MG, nullptr, rec_item + (size_t)t * (2 * MG + 2));
+                s0 = a.L;
+            }
+            if (mn == MG) fill_class_dev<MG>(a, f, at, c, s0, e - s0, rec_item);
+            else if (mn == MG - 1 && MG > 1) fill_class_dev<(MG > 1 ? MG - 1 : 1)>(a, f, at, c, s0, e - s0, rec_item);
+            else if (mn == MG - 2 && MG > 2) fill_class_dev<(MG > 2 ? MG - 2 : 1)>(a, f, at, c, s0, e - s0, rec_item);
+            s = e;
+            c++;
+        }
     }
 }
 
@@ -149,16 +179,30 @@ int rmfht_sample_maps(const rmfht_plan* p, uint64_t seed, long long frame0, long
     if (!p) return fail(RMFHT_EVALUE, "plan is NULL");
     if (B < 0) return fail(RMFHT_EVALUE, "negative batch");
     const int mg = p->m, S = p->S, M = p->M;
-    const long long total = B * (long long)M * S;
-    int err = 0;
-#pragma omp parallel for schedule(static) reduction(| : err)
-    for (long long i = 0; i < total; i++) {
-        const long long f = frame0 + i / ((long long)M * S);
-        const int a = (int)((i / S) % M), s = (int)(i % S);
-        rmfht_maps::table_entry(seed, f, a, s, p->L, p->sizes[s], mg, identity_root, raw ? raw + i * (mg + 1) : nullptr,
-                                rec ? rec + i * (2 * mg + 2) : nullptr);
+    const long long items = B * (long long)M;
+#pragma omp parallel for schedule(static)
+    for (long long item = 0; item < items; item++) {
+        const long long f = frame0 + item / M;
+        const int at = (int)(item % M);
+        uint16_t* raw_i = raw ? raw + (size_t)item * S * (mg + 1) : nullptr;
+        uint16_t* rec_i = rec ? rec + (size_t)item * S * (2 * mg + 2) : nullptr;
+        int s = 0, c = 0;
+        while (s < S) {
+            const int mn = p->sizes[s];
+            int e = s;
+            while (e < S && p->sizes[e] == mn) e++;
+            int s0 = s;
+            if (identity_root && at == 0 && s == 0) {
+                for (int t = 0; t < p->L; t++)
+                    rmfht_maps::write_identity(mn, mg, raw_i ? raw_i + (size_t)t * (mg + 1) : nullptr,
+                                               rec_i ? rec_i + (size_t)t * (2 * mg + 2) : nullptr);
+                s0 = p->L;
+            }
+            rmfht_maps::fill_class_host_any(mn, seed, f, at, c, s0, e - s0, mg, raw_i, rec_i);
+            s = e;
+            c++;
+        }
     }
-    (void)err;
     return 0;
 }
 
@@ -178,8 +222,8 @@ int rmfht_sample_maps_device(const rmfht_plan* p, uint64_t seed, long long frame
     a.m = p->m;
     a.identity_root = identity_root;
     for (int s = 0; s < p->S; s++) a.sizes[s] = (signed char)p->sizes[s];
-    const long long total = B * (long long)p->M * p->S;
-    long long blocks = (total + 255) / 256;
+    const long long warps = B * (long long)p->M;
+    long long blocks = (warps * 32 + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch (p->m) {

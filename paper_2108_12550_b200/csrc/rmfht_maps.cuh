@@ -156,41 +156,104 @@ RMFHT_HD void sample_map(uint64_t key, int mg, uint16_t* raw, uint16_t* rec) {
     }
 }
 
-// entry (frame f, attempt a, slot s) of a table: the identity for attempt
-// 0's L root maps when identity_root ("decoder 0 = identity"), else a fresh
-// draw keyed by (seed, f, a, s).  raw and/or rec may be null.
-template <int MN>
-RMFHT_HD void table_entry_t(uint64_t seed, long long f, int a, int s, int L, int mg, int identity_root, uint16_t* raw,
-                            uint16_t* rec) {
-    if (identity_root && a == 0 && s < L) {
-        if (raw) {
-            for (int k = 0; k <= mg; k++) raw[k] = 0;
-            for (int k = 0; k < MN; k++) raw[k] = (uint16_t)(1u << k);
-        }
-        if (rec) {
-            for (int k = 0; k < 2 * mg + 2; k++) rec[k] = 0;
-            for (int k = 0; k < MN; k++) {
-                rec[k] = (uint16_t)(1u << k);
-                rec[mg + 1 + k] = (uint16_t)(1u << k);
-            }
-        }
-        return;
-    }
-    const uint64_t key = seed * 0xD1B54A32D192ED03ull ^ ((uint64_t)f * 0x9E3779B97F4A7C15ull);
-    uint64_t st = key + ((uint64_t)a << 20) + (uint64_t)s;
-    sample_map<MN>(splitmix64(st), mg, raw, rec);
+// Table semantics (host and device): for each (frame f, attempt a), the
+// slots are filled class by class (a class = a run of slots with the same
+// map size, SURVEY §8(c) consumption order).  Candidate j of class c is
+// drawn from a counter-based stream keyed by (seed, f, a, c, j); invertible
+// candidates fill the class's slots in candidate order — the reference's own
+// rule (sample_affine_batch, automorphism.py:144-161: draw a batch, keep the
+// invertible ones in order).  With identity_root, attempt 0's L root slots
+// are the identity ("decoder 0 = identity") and are not drawn.
+RMFHT_HD uint64_t cand_key(uint64_t seed, long long f, int a, int c, long long j) {
+    uint64_t st = seed * 0xD1B54A32D192ED03ull ^ ((uint64_t)f * 0x9E3779B97F4A7C15ull);
+    st += ((uint64_t)a << 24) + ((uint64_t)c << 16);
+    uint64_t k = splitmix64(st);
+    k ^= (uint64_t)j * 0xC2B2AE3D27D4EB4Full;
+    return splitmix64(k);
 }
 
-RMFHT_HD void table_entry(uint64_t seed, long long f, int a, int s, int L, int mn, int mg, int identity_root,
-                          uint16_t* raw, uint16_t* rec) {
+// candidate j: row masks and shift; true if A is invertible (then inv holds A^-1)
+template <int MN>
+RMFHT_HD bool candidate(uint64_t key, unsigned (&rows)[MN], unsigned (&inv)[MN], unsigned& b) {
+    uint64_t st = key;
+    constexpr unsigned mask = (1u << MN) - 1u;
+    uint64_t w = 0;
+#pragma unroll
+    for (int r = 0; r < MN; r++) {
+        if (r % 4 == 0) w = splitmix64(st);
+        rows[r] = (unsigned)(w >> (16 * (r % 4))) & mask;
+    }
+    b = (unsigned)(splitmix64(st) & mask);
+    return gj_inverse<MN>(rows, inv);
+}
+
+template <int MN>
+RMFHT_HD void write_map(const unsigned (&rows)[MN], const unsigned (&inv)[MN], unsigned b, int mg, uint16_t* raw,
+                        uint16_t* rec) {
+    if (raw) {
+        for (int k = 0; k <= mg; k++) raw[k] = 0;
+#pragma unroll
+        for (int r = 0; r < MN; r++) raw[r] = (uint16_t)rows[r];
+        raw[mg] = (uint16_t)b;
+    }
+    if (rec) {
+        for (int k = 0; k < 2 * mg + 2; k++) rec[k] = 0;
+        unsigned cinv = 0;
+#pragma unroll
+        for (int k = 0; k < MN; k++) {
+            unsigned col = 0, icol = 0;
+#pragma unroll
+            for (int r = 0; r < MN; r++) {
+                col |= ((rows[r] >> k) & 1u) << r;
+                icol |= ((inv[r] >> k) & 1u) << r;
+            }
+            rec[k] = (uint16_t)col;
+            rec[mg + 1 + k] = (uint16_t)icol;
+            if ((b >> k) & 1u) cinv ^= icol;
+        }
+        rec[mg] = (uint16_t)b;
+        rec[2 * mg + 1] = (uint16_t)cinv;
+    }
+}
+
+RMFHT_HD void write_identity(int mn, int mg, uint16_t* raw, uint16_t* rec) {
+    if (raw) {
+        for (int k = 0; k <= mg; k++) raw[k] = 0;
+        for (int k = 0; k < mn; k++) raw[k] = (uint16_t)(1u << k);
+    }
+    if (rec) {
+        for (int k = 0; k < 2 * mg + 2; k++) rec[k] = 0;
+        for (int k = 0; k < mn; k++) {
+            rec[k] = (uint16_t)(1u << k);
+            rec[mg + 1 + k] = (uint16_t)(1u << k);
+        }
+    }
+}
+
+// host: one class of one (frame, attempt), sequential candidate order
+template <int MN>
+inline void fill_class_host(uint64_t seed, long long f, int a, int c, int s0, int cnt, int mg, uint16_t* raw,
+                            uint16_t* rec) {
+    int filled = 0;
+    for (long long j = 0; filled < cnt; j++) {
+        unsigned rows[MN], inv[MN], b;
+        if (!candidate<MN>(cand_key(seed, f, a, c, j), rows, inv, b)) continue;
+        const int s = s0 + filled++;
+        write_map<MN>(rows, inv, b, mg, raw ? raw + (size_t)s * (mg + 1) : nullptr,
+                      rec ? rec + (size_t)s * (2 * mg + 2) : nullptr);
+    }
+}
+
+inline void fill_class_host_any(int mn, uint64_t seed, long long f, int a, int c, int s0, int cnt, int mg,
+                                uint16_t* raw, uint16_t* rec) {
     switch (mn) {
-#define RMFHT_TE(K)                                                              \
-    case K:                                                                      \
-        table_entry_t<K>(seed, f, a, s, L, mg, identity_root, raw, rec); \
+#define RMFHT_FC(K)                                                   \
+    case K:                                                           \
+        fill_class_host<K>(seed, f, a, c, s0, cnt, mg, raw, rec); \
         break;
-        RMFHT_TE(1) RMFHT_TE(2) RMFHT_TE(3) RMFHT_TE(4) RMFHT_TE(5) RMFHT_TE(6) RMFHT_TE(7)
-        RMFHT_TE(8) RMFHT_TE(9) RMFHT_TE(10) RMFHT_TE(11) RMFHT_TE(12) RMFHT_TE(13) RMFHT_TE(14)
-#undef RMFHT_TE
+        RMFHT_FC(1) RMFHT_FC(2) RMFHT_FC(3) RMFHT_FC(4) RMFHT_FC(5) RMFHT_FC(6) RMFHT_FC(7)
+        RMFHT_FC(8) RMFHT_FC(9) RMFHT_FC(10) RMFHT_FC(11) RMFHT_FC(12) RMFHT_FC(13) RMFHT_FC(14)
+#undef RMFHT_FC
         default:
             break;
     }
