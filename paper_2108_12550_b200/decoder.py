@@ -236,3 +236,78 @@ def decode_batch(spec, alphas, L: int, M: int = 1, maps=None, seed: int | None =
         maps = plan.random_raw(alphas.shape[0], 0 if seed is None else seed)
     res = plan.decode(alphas, raw_maps=maps)
     return BatchResult(res["cw"], res["pm"], res["attempt"], res["path"])
+
+
+class StreamDecoder:
+    """Double-buffered host-to-host decoding: while batch k decodes on the
+    compute stream, batch k+1's LLRs copy in on a copy stream and batch k-1's
+    results copy out.  Permutation tables are drawn on the device from
+    (seed, frame offset), so only LLRs cross PCIe.
+
+        sd = StreamDecoder(plan, batch=16384, seed=777)
+        for llr in host_batches:            # pinned float32 [batch, N]
+            done = sd.submit(llr)           # results of an older batch, or None
+        rest = sd.drain()                   # results of the batches still in flight
+
+    Result dicts hold pinned host tensors (cw words, pm, attempt) that stay
+    valid until that buffer is reused `depth` submissions later.
+    """
+
+    def __init__(self, plan: Plan, batch: int, seed: int = 0, identity_root: bool = True, depth: int = 2):
+        torch = _torch()
+        self.torch, self.plan, self.batch, self.seed, self.ident = torch, plan, batch, seed, identity_root
+        dev = torch.device("cuda")
+        self.compute = torch.cuda.Stream()
+        self.copy = torch.cuda.Stream()
+        self.depth = depth
+        self.d_llr = [torch.empty((batch, plan.N), dtype=torch.float32, device=dev) for _ in range(depth)]
+        self.out = [plan.alloc_outputs(batch, dev) for _ in range(depth)]
+        self.h_out = [dict(cw=torch.empty((batch, plan.words), dtype=torch.int32).pin_memory(),
+                           pm=torch.empty(batch, dtype=torch.float32).pin_memory(),
+                           attempt=torch.empty(batch, dtype=torch.int32).pin_memory()) for _ in range(depth)]
+        self.in_ready = [torch.cuda.Event() for _ in range(depth)]
+        self.done = [torch.cuda.Event() for _ in range(depth)]
+        self.out_ready = [torch.cuda.Event() for _ in range(depth)]
+        self.pending = []
+        self.k = 0
+        self.frame0 = 0
+
+    def submit(self, h_llr):
+        """Queue one pinned host batch (torch tensor [n <= batch, N])."""
+        torch = self.torch
+        i = self.k % self.depth
+        n = h_llr.shape[0]
+        ready = None
+        if len(self.pending) >= self.depth:
+            j, ev, nj = self.pending.pop(0)
+            ev.synchronize()
+            ready = {k: v[:nj] for k, v in self.h_out[j].items()}
+        with torch.cuda.stream(self.copy):
+            self.copy.wait_event(self.done[i])  # buffer i free (its previous decode finished)
+            self.d_llr[i][:n].copy_(h_llr, non_blocking=True)
+            self.in_ready[i].record(self.copy)
+        with torch.cuda.stream(self.compute):
+            self.compute.wait_event(self.in_ready[i])
+            self.compute.wait_event(self.out_ready[i])  # previous results of buffer i copied out
+            out = {k: v[:n] for k, v in self.out[i].items()}
+            self.plan.launch_sampled(self.d_llr[i][:n], self.seed, out, frame0=self.frame0,
+                                     identity_root=self.ident, stream=self.compute)
+            self.done[i].record(self.compute)
+        with torch.cuda.stream(self.copy):
+            self.copy.wait_event(self.done[i])
+            for key in ("cw", "pm", "attempt"):
+                self.h_out[i][key][:n].copy_(self.out[i][key][:n], non_blocking=True)
+            self.out_ready[i].record(self.copy)
+        self.pending.append((i, self.out_ready[i], n))
+        self.k += 1
+        self.frame0 += n
+        return ready
+
+    def drain(self):
+        """Wait for all queued batches; returns the last `depth` batches' host results."""
+        res = []
+        for i, ev, n in self.pending:
+            ev.synchronize()
+            res.append({k: v[:n] for k, v in self.h_out[i].items()})
+        self.pending = []
+        return res

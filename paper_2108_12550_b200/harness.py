@@ -1,0 +1,306 @@
+"""Batched Monte Carlo FER harness on the GPU.
+
+A drop-in for the reference's ``harness.run_job`` on the p-FHT-FSCL family
+(``harness.py:116-165``): the same ``SimJob`` / ``FerRecord`` fields and CSV
+schema (``harness.py:26-29,198-262``), the same stopping rule (after each
+round of batches, stop once ``min_frame_errors`` is reached), the same
+ML-lower-bound rule (``harness.py:79-84``).  Differences, by design:
+
+* frames are decoded in GPU batches instead of 250-frame CPU chunks;
+* frames are drawn per batch from counter-keyed generators (seed, point,
+  batch) and permutation tables per frame from (seed, point, frame), so a
+  run is identical for any number of ranks (the reference's
+  worker-determinism property, ``test_acceptance.py:306-318``);
+* ranks shard the batches (round-robin); the only collective is one sum
+  of three counters per round (``torch.distributed``; NCCL or gloo).
+
+``decode_fn`` is injectable for tests (e.g. the CPU oracle on gloo ranks);
+the default is the CUDA decoder.
+"""
+
+from __future__ import annotations
+
+import csv
+import io
+import json
+import time
+from dataclasses import asdict, dataclass
+from math import ceil, log2
+
+import numpy as np
+
+from .channel_model import ChannelConfig
+from .plan import complexity_ops, plan_visits
+from .rm_core import ConfigurationError, build_code, polar_transform
+from .top_decoders import SUPPORTED, DecoderConfig
+
+CSV_HEADER = ["r", "m", "decoder", "L", "M", "P", "ebn0_db", "frames",
+              "frame_errors", "fer", "ml_lb_fer", "avg_additions",
+              "avg_comparisons", "time_steps", "mem_bits", "wall_seconds",
+              "seed"]
+
+
+@dataclass(frozen=True)
+class SimJob:
+    """harness.py:34-56 (plus the GPU batch size)."""
+    r: int
+    m: int
+    decoder: DecoderConfig
+    ebn0_points: tuple
+    max_frames: int = 10000
+    min_frame_errors: int = 100
+    seed: int = 0
+    workers: int = 1
+    zero_noise: bool = False
+    batch: int = 65536
+
+    def __post_init__(self):
+        if self.max_frames < 1:
+            raise ConfigurationError("max_frames must be >= 1")
+        pts = tuple(float(p) for p in self.ebn0_points)
+        if not pts or any(b <= a for a, b in zip(pts, pts[1:])):
+            raise ConfigurationError("ebn0_points must be nonempty and strictly increasing")
+        object.__setattr__(self, "ebn0_points", pts)
+        build_code(self.r, self.m)
+        if self.decoder.algorithm not in SUPPORTED:
+            raise ConfigurationError(f"algorithm {self.decoder.algorithm!r} is not part of this decoder "
+                                     f"(supported: {', '.join(SUPPORTED)})")
+        if self.batch < 1:
+            raise ConfigurationError("batch must be >= 1")
+
+
+@dataclass
+class FerRecord:
+    """harness.py:58-76"""
+    r: int
+    m: int
+    decoder: str
+    L: int
+    M: int
+    P: int
+    ebn0_db: float
+    frames: int
+    frame_errors: int
+    fer: float
+    ml_lb_fer: float
+    avg_additions: float
+    avg_comparisons: float
+    time_steps: int
+    mem_bits: int
+    wall_seconds: float
+    seed: int
+
+
+# --------------------------------------------------------------- cost model
+# Restated from accounting.py for the supported family: the modeled figures
+# the reference writes into every FerRecord.
+
+def modeled_cost(r: int, m: int, cfg: DecoderConfig):
+    """(ops, time_steps, mem_bits): complexity_model, latency_total,
+    memory_model (accounting.py:189-227, 323-347)."""
+    algo = cfg.algorithm
+    perms = algo == "p-FHT-FSCL"
+    ops = complexity_ops(r, m, cfg.L if algo != "FHT-FSC" else 1, cfg.M if perms else 1, perms,
+                         include_perm=False, fsc=algo == "FHT-FSC")
+    eff_l = 1 if algo == "FHT-FSC" else cfg.L
+
+    def msteps(n):
+        return int(ceil(log2(n))) if n > 1 else 0
+
+    steps = 0
+    for kind, mm in plan_visits(r, m, perms):
+        n = 1 << mm
+        if kind in ("f", "g"):
+            steps += 1
+        elif kind == "fht":
+            steps += mm + msteps(eff_l * min(eff_l, n))
+        elif kind == "spc":
+            steps += mm if eff_l == 1 else mm + (min(eff_l, n) - 1) + msteps(2 * eff_l)
+        elif kind == "perm":
+            steps += 2 + msteps(2 * eff_l)
+    steps += msteps(eff_l)
+    if perms and cfg.M > 1:
+        steps += msteps(cfg.M)
+    N, Q, L, M = 1 << m, 32, cfg.L, cfg.M
+    if algo == "FHT-FSC":
+        mem = (2 * N - 1) * Q + N
+    elif not perms:
+        mem = N * (L + 1) * Q + 2 * L * Q + 2 * N * L
+    elif L == 1 and M == 1:
+        mem = (2 * N + 1) * Q + N
+    elif L == 1:
+        mem = (N + M * (N + 1)) * Q + M * N
+    elif M == 1:
+        mem = N * (L + 1) * Q + 2 * L * Q + 2 * N * L
+    else:
+        mem = N * (L * M + 1) * Q + 2 * M * L * Q + 2 * M * N * L
+    return ops, steps, mem
+
+
+def split_ops(r: int, m: int, cfg: DecoderConfig, total: int):
+    """harness._split_ops (harness.py:233-256): additions vs comparisons."""
+    perms = cfg.algorithm == "p-FHT-FSCL"  # the model follows the algorithm's flags (accounting._ALGO_FLAGS)
+    eff_l = 1 if cfg.algorithm == "FHT-FSC" else cfg.L
+    comps = 0
+    for kind, mm in plan_visits(r, m, perms):
+        if kind == "f":
+            comps += eff_l * (1 << (mm - 1))
+        elif kind == "fht":
+            comps += eff_l * (1 << mm) + int(2 * eff_l * eff_l * np.log2(eff_l))
+        elif kind == "spc":
+            n = 1 << mm
+            if eff_l == 1:
+                comps += n
+            else:
+                tau = min(eff_l, n)
+                comps += min(eff_l * mm * n, eff_l * eff_l * n) + int(2 * tau * eff_l * (1 + log2(eff_l)))
+    comps = min(comps, total)
+    return total - comps, comps
+
+
+# ----------------------------------------------------------------- frames
+
+def batch_frames(spec, chan: ChannelConfig, seed: int, point: int, batch_index: int, size: int,
+                 zero_noise: bool = False):
+    """Frames of one batch, keyed by (seed, point, batch): uniform info
+    bits, polar encoding, BPSK + AWGN, float32 LLR = 2y/sigma^2."""
+    rng = np.random.default_rng(np.random.SeedSequence((int(seed), int(point), int(batch_index), 0x4D43)))
+    u = np.zeros((size, spec.N), dtype=np.uint8)
+    u[:, list(spec.info_set)] = rng.integers(0, 2, size=(size, spec.K), dtype=np.uint8)
+    x = polar_transform(u)
+    y = 1.0 - 2.0 * x
+    if not zero_noise:
+        y = y + chan.sigma * rng.standard_normal((size, spec.N))
+    return x, (2.0 * y / chan.sigma ** 2).astype(np.float32)
+
+
+def _table_seed(seed: int, point: int) -> int:
+    return (int(seed) * 1000003 + int(point) * 7919 + 0x5EED) & ((1 << 63) - 1)
+
+
+class GpuDecoder:
+    """Default decode_fn: the CUDA decoder with on-device permutation tables."""
+
+    def __init__(self, spec, cfg: DecoderConfig, device=None):
+        import torch
+        from .decoder import Plan
+        self.torch = torch
+        perms = cfg.algorithm == "p-FHT-FSCL" and cfg.permutations_enabled
+        L = 1 if cfg.algorithm == "FHT-FSC" else cfg.L
+        self.plan = Plan(spec.r, spec.m, L, cfg.M if perms else 1, perms, "f32")
+        self.perms = perms
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+
+    def __call__(self, llr: np.ndarray, table_seed: int, frame0: int):
+        torch = self.torch
+        d_llr = torch.from_numpy(llr).to(self.device)
+        out = self.plan.alloc_outputs(llr.shape[0], self.device)
+        if self.perms:
+            self.plan.launch_sampled(d_llr, table_seed, out, frame0=frame0, identity_root=True)
+        else:
+            self.plan.launch(d_llr, None, out)
+        words = out["cw"].cpu().numpy().view(np.uint32)
+        bits = np.unpackbits(words.view(np.uint8), axis=-1, bitorder="little")[:, :llr.shape[1]]
+        return bits
+
+
+def _allreduce(vals, group):
+    import torch
+    import torch.distributed as dist
+    backend = dist.get_backend(group) if group is not None else dist.get_backend()
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    t = torch.tensor(vals, dtype=torch.int64, device=dev)
+    dist.all_reduce(t, group=group)
+    return [int(v) for v in t.cpu().tolist()]
+
+
+def run_job(job: SimJob, decode_fn=None, rank: int = 0, world: int = 1, group=None) -> list:
+    """Simulate every SNR point; returns one FerRecord each (harness.py:116-165)."""
+    spec = build_code(job.r, job.m)
+    cfg = job.decoder
+    ops, steps, mem = modeled_cost(job.r, job.m, cfg)
+    adds, comps = split_ops(job.r, job.m, cfg, ops)
+    if decode_fn is None:
+        decode_fn = GpuDecoder(spec, cfg)
+    nb_total = -(-job.max_frames // job.batch)
+    records = []
+    for q, ebn0 in enumerate(job.ebn0_points):
+        chan = ChannelConfig.for_rate(ebn0, spec.rate, job.seed)
+        tseed = _table_seed(job.seed, q)
+        t0 = time.monotonic()
+        frames = errors = ml_errors = 0
+        b = 0
+        while b < nb_total:
+            my = [bi for bi in range(b, min(b + world, nb_total)) if bi % world == rank]
+            loc = [0, 0, 0]
+            for bi in my:
+                size = min(job.batch, job.max_frames - bi * job.batch)
+                x, llr = batch_frames(spec, chan, job.seed, q, bi, size, job.zero_noise)
+                xhat = decode_fn(llr, tseed, bi * job.batch)
+                wrong = np.any(xhat != x, axis=1)
+                if wrong.any():
+                    a = llr[wrong].astype(np.float64)
+                    c_hat = np.sum((1.0 - 2.0 * xhat[wrong]) * a, axis=1)   # correlation (top_decoders.py:231)
+                    c_tx = np.sum((1.0 - 2.0 * x[wrong]) * a, axis=1)
+                    ml = int(np.sum(c_hat >= c_tx))
+                else:
+                    ml = 0
+                loc[0] += size
+                loc[1] += int(wrong.sum())
+                loc[2] += ml
+            if world > 1:
+                loc = _allreduce(loc, group)
+            frames += loc[0]
+            errors += loc[1]
+            ml_errors += loc[2]
+            b += world
+            if errors >= job.min_frame_errors:
+                break
+        wall = time.monotonic() - t0
+        records.append(FerRecord(
+            r=job.r, m=job.m, decoder=cfg.algorithm, L=cfg.L, M=cfg.M, P=cfg.P, ebn0_db=float(ebn0),
+            frames=frames, frame_errors=errors, fer=errors / frames, ml_lb_fer=ml_errors / frames,
+            avg_additions=float(adds), avg_comparisons=float(comps), time_steps=steps, mem_bits=mem,
+            wall_seconds=wall, seed=job.seed))
+    return records
+
+
+# ------------------------------------------------------------ persistence
+def _fmt(value):
+    return repr(value) if isinstance(value, float) else value
+
+
+def records_to_csv(records) -> str:
+    """harness.py:198-206"""
+    buf = io.StringIO()
+    w = csv.writer(buf, lineterminator="\n")
+    w.writerow(CSV_HEADER)
+    for rec in records:
+        row = asdict(rec)
+        w.writerow([_fmt(row[k]) for k in CSV_HEADER])
+    return buf.getvalue()
+
+
+def records_to_json(records) -> str:
+    return json.dumps([asdict(r) for r in records], indent=1)
+
+
+def parse_csv(text: str) -> list:
+    out = []
+    for row in csv.DictReader(io.StringIO(text)):
+        out.append(FerRecord(
+            r=int(row["r"]), m=int(row["m"]), decoder=row["decoder"], L=int(row["L"]), M=int(row["M"]),
+            P=int(row["P"]), ebn0_db=float(row["ebn0_db"]), frames=int(row["frames"]),
+            frame_errors=int(row["frame_errors"]), fer=float(row["fer"]), ml_lb_fer=float(row["ml_lb_fer"]),
+            avg_additions=float(row["avg_additions"]), avg_comparisons=float(row["avg_comparisons"]),
+            time_steps=int(row["time_steps"]), mem_bits=int(row["mem_bits"]),
+            wall_seconds=float(row["wall_seconds"]), seed=int(row["seed"])))
+    return out
+
+
+def clopper_pearson(k: int, n: int, alpha: float = 0.05):
+    """Exact binomial interval (FER interval)."""
+    from scipy.stats import beta
+    lo = 0.0 if k == 0 else float(beta.ppf(alpha / 2, k, n - k + 1))
+    hi = 1.0 if k == n else float(beta.ppf(1 - alpha / 2, k + 1, n - k))
+    return lo, hi

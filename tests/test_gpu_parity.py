@@ -163,3 +163,27 @@ def test_sampled_decode_matches_table_decode():
     assert np.array_equal(out["cw"].cpu().numpy().view(np.uint32), a["cw_packed"])
     assert np.array_equal(out["pm"].cpu().numpy(), a["pm"])
     assert np.array_equal(out["attempt"].cpu().numpy(), a["attempt"])
+
+
+def test_stream_decoder_matches_direct_launch():
+    import torch
+    from paper_2108_12550_b200.channel_model import synthetic_frames
+    from paper_2108_12550_b200.decoder import Plan, StreamDecoder
+    from paper_2108_12550_b200.rm_core import build_code
+    spec = build_code(2, 7)
+    plan = Plan(2, 7, 2, 4, True, "f32")
+    batches = [synthetic_frames(spec, 2.0, 1000, seed=s)[1] for s in range(5)]
+    sd = StreamDecoder(plan, 1000, seed=31)
+    got = []
+    for llr in batches:
+        r = sd.submit(torch.from_numpy(llr).pin_memory())
+        if r is not None:
+            got.append({k: v.clone() for k, v in r.items()})
+    got += [{k: v.clone() for k, v in r.items()} for r in sd.drain()]
+    assert len(got) == 5
+    for i, llr in enumerate(batches):
+        _, rec = plan.sample(1000, seed=31, frame0=1000 * i)
+        ref = plan.decode(llr, records=rec)
+        assert np.array_equal(got[i]["cw"].numpy().view(np.uint32), ref["cw_packed"])
+        assert np.array_equal(got[i]["pm"].numpy(), ref["pm"])
+        assert np.array_equal(got[i]["attempt"].numpy(), ref["attempt"])
