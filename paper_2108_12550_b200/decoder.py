@@ -249,8 +249,7 @@ class StreamDecoder:
             done = sd.submit(llr)           # results of an older batch, or None
         rest = sd.drain()                   # results of the batches still in flight
 
-    Result dicts hold pinned host tensors (cw words, pm, attempt) that stay
-    valid until that buffer is reused `depth` submissions later.
+    Result dicts hold host tensors (cw words, pm, attempt) owned by the caller.
     """
 
     def __init__(self, plan: Plan, batch: int, seed: int = 0, identity_root: bool = True, depth: int = 2):
@@ -281,7 +280,8 @@ class StreamDecoder:
         if len(self.pending) >= self.depth:
             j, ev, nj = self.pending.pop(0)
             ev.synchronize()
-            ready = {k: v[:nj] for k, v in self.h_out[j].items()}
+            # buffer j is reused right below: hand out a snapshot
+            ready = {k: v[:nj].clone() for k, v in self.h_out[j].items()}
         with torch.cuda.stream(self.copy):
             self.copy.wait_event(self.done[i])  # buffer i free (its previous decode finished)
             self.d_llr[i][:n].copy_(h_llr, non_blocking=True)
@@ -308,6 +308,6 @@ class StreamDecoder:
         res = []
         for i, ev, n in self.pending:
             ev.synchronize()
-            res.append({k: v[:n] for k, v in self.h_out[i].items()})
+            res.append({k: v[:n].clone() for k, v in self.h_out[i].items()})
         self.pending = []
         return res
