@@ -66,6 +66,11 @@ __device__ __forceinline__ u64 sub2(u64 a, u64 b) {
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
     return r;
 }
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+    u64 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
 __device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
     u64 r;
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
@@ -94,7 +99,6 @@ struct Lv {
 template <int R, int MM, int L>
 struct alignas(16) WS2 {
     using C = Cfg<R, MM, L>;
-    float alpha[C::N];          // this warp's frame LLRs
     float lmp[2 * L][32];       // LM lane partials per trial
     MapS maps[C::S > 0 ? C::S : 1];
     MapS comp[L];     // composite map of each root path (root perm-ext winners)
@@ -133,6 +137,7 @@ struct Ctx2 {
     const float* alpha;        // frame LLRs (shared memory)
     float ach[C::NS];          // channel layout: ach[s] = alpha[lane + 32 s]
     int lane, p, u;
+    u32 alpha_saddr;           // shared-window address of alpha (2 KB aligned)
 };
 
 // ------------------------------------------------------------ helpers ----
@@ -166,12 +171,14 @@ struct RootIdx {
     static constexpr int NA = V < 8 ? V : 8;
     static constexpr int NB = V / NA;
     u32 base, A[NA], B[NB];
-    __device__ __forceinline__ void build(const MapS& mp, int u) {
+    // alpha_saddr: shared-window address of the frame LLRs, aligned to 2 KB so
+    // that XOR-ing byte offsets (< 2 KB) into it forms the address directly
+    __device__ __forceinline__ void build(const MapS& mp, int u, u32 alpha_saddr) {
         constexpr int LB = clog2(LPP);
         u32 bse = mp.c;
 #pragma unroll
         for (int b = 0; b < LB; b++) bse ^= (u >> b & 1) ? mp.icol[b] : 0u;
-        base = bse << 2;
+        base = alpha_saddr | (bse << 2);
         A[0] = 0;
 #pragma unroll
         for (int i = 1; i < NA; i++) {
@@ -190,6 +197,12 @@ struct RootIdx {
 
 __device__ __forceinline__ float lds_byte(const float* base, u32 byteoff) {
     return *reinterpret_cast<const float*>(reinterpret_cast<const char*>(base) + byteoff);
+}
+// load from a 32-bit shared-window address (the gather tables carry the base)
+__device__ __forceinline__ float lds_addr(u32 saddr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(saddr));
+    return v;
 }
 
 // Rare path of fht_node (more candidates than kCap): exact K-round selection
@@ -813,6 +826,39 @@ __device__ __forceinline__ void perm_ext_inner2(Ctx2<R, MM, L>& cx, float (&x)[L
     __syncwarp();
 }
 
+
+// g (list_engine.py:23-27) when the left child is an FHT node: its hard
+// decisions for this lane are bit_k = c0 ^ parity(Bh & k) (fht_node), so
+// the +-1 factors follow a Gray-code walk: one FMUL2 + one FFMA2 per pair.
+template <int R, int MM, int L, int SS>
+__device__ __forceinline__ void g_fht_child(const Ctx2<R, MM, L>& cx, int slot, const float* a, const float* b,
+                                            float* out) {
+    using C = Cfg<R, MM, L>;
+    using LV = Lv<SS, C::LPP>;  // the left child's level
+    constexpr int V = LV::V, n = LV::n;
+    static_assert(LV::full && V >= 2, "paired walk");
+    const int bin = cx.ws.sel_bin[slot];
+    const int sgn = cx.ws.sel_w[slot] < 0.f;
+    const u32 B = (u32)(~bin) & (u32)(n - 1);
+    const u32 Bh = B >> C::LB;
+    const int c0 = sgn ^ (__popc(B) & 1) ^ (__popc(B & (u32)cx.u & (u32)(C::LPP - 1)) & 1);
+    const float base = c0 ? -1.f : 1.f;
+    const float col0 = (Bh & 1u) ? -1.f : 1.f;
+    u64 s2 = pk(base, base * col0);  // factors of slots (k, k+1), k = 2 * gray(i)
+#pragma unroll
+    for (int i = 0; i < V / 2; i++) {
+        if (i > 0) {
+            const int j = __ffs(i);  // bit of k flipped by this Gray step (>= 1)
+            const float cj = ((Bh >> j) & 1u) ? -1.f : 1.f;
+            s2 = mul2(s2, pk(cj, cj));
+        }
+        const int k = 2 * (i ^ (i >> 1));
+        const u64 r = fma2(s2, pk(a[k], a[k + 1]), pk(b[k], b[k + 1]));
+        out[k] = plo(r);
+        out[k + 1] = phi(r);
+    }
+}
+
 // ------------------------------------------------------- tree recursion ----
 template <int R, int MM, int L, int RR, int SS, bool SPINE>
 __device__ __forceinline__ u64 node2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_t* lin) {
@@ -856,7 +902,9 @@ __device__ __forceinline__ u64 node2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / 
         }
         // g (:104) with the left child's hard decisions
         float xr[VC];
-        if constexpr (LC::full) {
+        if constexpr (RR - 1 == 1 && LC::full && VC >= 2) {
+            g_fht_child<R, MM, L, SS - 1>(cx, p, x, x + VC, xr);
+        } else if constexpr (LC::full) {
 #pragma unroll
             for (int k = 0; k < VC; k++) {
                 const float sg = ((bl >> k) & 1ull) ? -1.f : 1.f;
@@ -922,26 +970,35 @@ __device__ __forceinline__ u64 root_node(Ctx2<R, MM, L>& cx, int8_t* lin) {
     static_assert(LC::full, "root children span the lane group");
     auto& ws = cx.ws;
     const int lane = cx.lane, p = cx.p, u = cx.u;
-    const float* alpha = ws.alpha;
     int8_t* l0 = ws.l0[MM];
     int8_t* l1 = ws.l1[MM];
     int8_t* l2 = ws.l2[MM];
     float xl[VC];
     {
         RootIdx<MM, C::LPP, LV::V> ri;
-        ri.build(ws.comp[p], u);
+        ri.build(ws.comp[p], u, cx.alpha_saddr);
 #pragma unroll
-        for (int k = 0; k < VC; k++) xl[k] = f_op(lds_byte(alpha, ri.off(k)), lds_byte(alpha, ri.off(k + VC)));
+        for (int k = 0; k < VC; k++) xl[k] = f_op(lds_addr(ri.off(k)), lds_addr(ri.off(k + VC)));
     }
     const u64 bl = node2<R, MM, L, R - 1, MM - 1, true>(cx, xl, l1);
     float xr[VC];
     {
         RootIdx<MM, C::LPP, LV::V> ri;
-        ri.build(ws.comp[l1[p]], u);
+        ri.build(ws.comp[l1[p]], u, cx.alpha_saddr);
+        if constexpr (R - 1 == 1 && VC >= 2) {
+            float ga[VC], gb[VC];
 #pragma unroll
-        for (int k = 0; k < VC; k++) {
-            const float sg = ((bl >> k) & 1ull) ? -1.f : 1.f;
-            xr[k] = __fmaf_rn(sg, lds_byte(alpha, ri.off(k)), lds_byte(alpha, ri.off(k + VC)));
+            for (int k = 0; k < VC; k++) {
+                ga[k] = lds_addr(ri.off(k));
+                gb[k] = lds_addr(ri.off(k + VC));
+            }
+            g_fht_child<R, MM, L, MM - 1>(cx, p, ga, gb, xr);
+        } else {
+#pragma unroll
+            for (int k = 0; k < VC; k++) {
+                const float sg = ((bl >> k) & 1ull) ? -1.f : 1.f;
+                xr[k] = __fmaf_rn(sg, lds_addr(ri.off(k)), lds_addr(ri.off(k + VC)));
+            }
         }
     }
     const u64 br = node2<R, MM, L, R, MM - 1, false>(cx, xr, l2);
@@ -975,10 +1032,16 @@ __global__ void __launch_bounds__(512, 1) decode_kernel2(rmfht::Params<float> pr
     constexpr int N = C::N, S = C::S, REC = 2 * MM + 2, V = LV::V;
     static_assert(N >= 32 && L <= 8 && N <= 512, "fast kernel: 32 <= N <= 512, L <= 8");
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    WS* wsarr = reinterpret_cast<WS*>(smem_raw);
     const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = lane_id();
+    // per-warp frame LLRs, each 2 KB aligned in the shared window, then the scratch
+    const u32 raw_saddr = (u32)__cvta_generic_to_shared(smem_raw);
+    const u32 pad = ((raw_saddr + 2047u) & ~2047u) - raw_saddr;
+    constexpr u32 ASTRIDE = ((u32)N * 4u + 2047u) & ~2047u;
+    float* alpha_w = reinterpret_cast<float*>(smem_raw + pad + (size_t)warp * ASTRIDE);
+    WS* wsarr = reinterpret_cast<WS*>(smem_raw + pad + (size_t)nwarps * ASTRIDE);
     WS& ws = wsarr[warp];
-    Ctx2<R, MM, L> cx{ws, ws.alpha, {}, lane, lane / C::LPP, lane % C::LPP};
+    Ctx2<R, MM, L> cx{ws, alpha_w, {}, lane, lane / C::LPP, lane % C::LPP,
+                      (u32)__cvta_generic_to_shared(alpha_w)};
     constexpr bool ROOT_INTERNAL = !(R == 1 || R == MM - 1);
     const long long items = prm.B * (long long)prm.M;
     long long cur_f = -1;
@@ -989,10 +1052,10 @@ __global__ void __launch_bounds__(512, 1) decode_kernel2(rmfht::Params<float> pr
             const int a = (int)(item % prm.M);
             if (f != cur_f) {
                 const float4* src4 = reinterpret_cast<const float4*>(prm.llr + f * N);
-                for (int i = lane; i < N / 4; i += 32) reinterpret_cast<float4*>(ws.alpha)[i] = src4[i];
+                for (int i = lane; i < N / 4; i += 32) reinterpret_cast<float4*>(alpha_w)[i] = src4[i];
                 __syncwarp();
 #pragma unroll
-                for (int s = 0; s < C::NS; s++) cx.ach[s] = ws.alpha[lane + 32 * s];
+                for (int s = 0; s < C::NS; s++) cx.ach[s] = alpha_w[lane + 32 * s];
                 cur_f = f;
             }
             const uint16_t* recs = prm.maps + (size_t)item * S * REC;
@@ -1017,9 +1080,9 @@ __global__ void __launch_bounds__(512, 1) decode_kernel2(rmfht::Params<float> pr
             } else {
                 float x[V];
                 RootIdx<MM, C::LPP, V> ri;
-                ri.build(ws.comp[cx.p], cx.u);
+                ri.build(ws.comp[cx.p], cx.u, cx.alpha_saddr);
 #pragma unroll
-                for (int k = 0; k < V; k++) x[k] = lds_byte(ws.alpha, ri.off(k));
+                for (int k = 0; k < V; k++) x[k] = lds_addr(ri.off(k));
                 bits = node2<R, MM, L, R, MM, true>(cx, x, rlin);
             }
             // best path: first minimum (:152)
@@ -1123,7 +1186,9 @@ __global__ void __launch_bounds__(256) reduce_kernel2(rmfht::Params<float> prm, 
 
 template <int R, int MM, int L>
 constexpr size_t smem_bytes2(int nwarps) {
-    return sizeof(WS2<R, MM, L>) * size_t(nwarps);
+    // 2 KB alignment pad + per-warp LLR copies + per-warp scratch
+    return 2048 + ((size_t(1 << MM) * 4 + 2047) & ~size_t(2047)) * size_t(nwarps) +
+           sizeof(WS2<R, MM, L>) * size_t(nwarps);
 }
 
 template <int R, int MM, int L>
