@@ -119,7 +119,7 @@ struct alignas(16) WS2 {
     int8_t l0[MM + 1][L], l1[MM + 1][L], l2[MM + 1][L], rootchain[L], ord[2 * L];
     int16_t nmap[MM + 1][L];
     // SPC scratch: magnitudes, signs, order of the tau+1 least reliable positions
-    float smag[L * C::SPCMAX];
+    float smag[L * (C::SPCMAX > 16 ? C::SPCMAX : 16)];
     uint8_t ssgn[L * C::SPCMAX];
     uint16_t sord[L * 16];
     float vbuf[R >= 3 ? L * C::N : 1];  // inner permutation nodes
@@ -376,11 +376,38 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
         for (int k = 0; k < V; k++) ws.wsp[lane][k] = w[k];
     }
     __syncwarp();
-    if (total <= kCap) {
-        // candidates per path (for the per-path top-K rule, fht_decode.py:116)
-        int pcnt = cnt;
+    // candidates per path (for the per-path top-K rule, fht_decode.py:116)
+    int pcnt = cnt;
 #pragma unroll
-        for (int off = 1; off < LV::act; off <<= 1) pcnt += __shfl_xor_sync(kFull, pcnt, off);
+    for (int off = 1; off < LV::act; off <<= 1) pcnt += __shfl_xor_sync(kFull, pcnt, off);
+    if (__all_sync(kFull, pcnt == 1)) {
+        // common case: every path's only candidate is its maximum, so the
+        // pool is the L path maxima ordered by (pm, source slot) (:116-120)
+        const u32 bal = __ballot_sync(kFull, cnt > 0);
+        const int owner = __ffs((bal >> (p * C::LPP)) & ((LV::act >= 32) ? 0xffffffffu : ((1u << LV::act) - 1u))) - 1;
+        int mybin = 0;
+        float myw = 0.f;
+        if (cnt > 0) {
+            const int k = (sizeof(MaskT) == 8 ? __ffsll((long long)mask) : __ffs((int)mask)) - 1;
+            mybin = LV::full ? k * C::LPP + u : u;
+            myw = ws.wsp[lane][k];
+        }
+        const int bin = __shfl_sync(kFull, mybin, p * C::LPP + owner);
+        const float wv = __shfl_sync(kFull, myw, p * C::LPP + owner);
+        int rank = 0;
+#pragma unroll
+        for (int q = 0; q < L; q++) {
+            const float cq = __shfl_sync(kFull, cbest, q * C::LPP);
+            rank += (cq < cbest) || (cq == cbest && q < p);
+        }
+        if (u == 0) {
+            ws.sel_src[rank] = p;
+            ws.sel_bin[rank] = bin;
+            ws.sel_w[rank] = wv;
+            ws.sel_pm[rank] = cbest;
+        }
+        __syncwarp();
+    } else if (total <= kCap) {
         const bool over = __any_sync(kFull, pcnt > K);
         int pos = incl - cnt;
         // this path's candidates occupy [pstart, pstart + pcnt) (lane order)
@@ -495,10 +522,106 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
     return act ? bits : 0ull;
 }
 
+// spc_decode_list (list_engine.py:68-119) for nodes with one element per
+// lane (n <= lanes per path): list state in lanes (slot i in lane i), ranks
+// by shuffles, signs by ballot.
+template <int R, int MM, int L, int SS>
+__device__ __forceinline__ u64 spc_node_v1(Ctx2<R, MM, L>& cx, float xv, int8_t* lin) {
+    using C = Cfg<R, MM, L>;
+    using LV = Lv<SS, C::LPP>;
+    constexpr int n = LV::n;
+    constexpr int TAU = cmin(cmin(L, n), n - 1);
+    static_assert(LV::V == 1 && n <= 32, "one element per lane");
+    auto& ws = cx.ws;
+    const int lane = cx.lane, p = cx.p, u = cx.u;
+    const bool act = u < n;
+    const float mag = act ? fabsf(xv) : 0.f;
+    const u32 sbal = __ballot_sync(kFull, act && xv < 0.f);  // hard decisions (:84)
+    constexpr u32 AM = (n >= 32) ? 0xffffffffu : ((1u << n) - 1u);
+    // stable ascending rank of |alpha| inside the path (:83)
+    int rank = 0;
+#pragma unroll
+    for (int v = 1; v < n; v++) {
+        const int w = (u + v) % n;
+        const float mw = __shfl_sync(kFull, mag, p * C::LPP + w);
+        rank += (mw < mag) || (mw == mag && w < u);
+    }
+    if (act && rank <= TAU) {
+        ws.smag[p * 16 + rank] = mag;
+        ws.sord[p * 16 + rank] = (uint16_t)u;
+    }
+    __syncwarp();
+    // slot state (lane i < L holds slot i): metric, running parity, parent path, flips
+    float spm = 0.f, spar = 0.f;
+    int sparent = 0, sfl = 0;
+    if (lane < L) {
+        const int par0 = __popc((sbal >> (lane * C::LPP)) & AM) & 1;
+        spm = ws.pm[lane] + (par0 ? ws.smag[lane * 16] : 0.f);  // :88
+        spar = (float)par0;
+        sparent = lane;
+    }
+#pragma unroll 1
+    for (int j = 1; j <= TAU; j++) {  // :97-112
+        const int i = lane >> 1;
+        const float ipm = __shfl_sync(kFull, spm, i);
+        const float ipar = __shfl_sync(kFull, spar, i);
+        const int ipa = __shfl_sync(kFull, sparent, i);
+        const int ifl = __shfl_sync(kFull, sfl, i);
+        float cand = 3.4e38f;
+        if (lane < 2 * L) {
+            if (lane & 1) {
+                const float t = ipm + ws.smag[ipa * 16 + j];
+                const float am = ws.smag[ipa * 16];
+                cand = ipar != 0.f ? t - am : t + am;  // pms + a_j + (1 - 2 par) a_m
+            } else {
+                cand = ipm;
+            }
+        }
+        int r2 = 0;
+#pragma unroll
+        for (int c = 0; c < 2 * L; c++) {
+            const float cc = __shfl_sync(kFull, cand, c);
+            r2 += (cc < cand) || (cc == cand && c < lane);
+        }
+        if (lane < 2 * L && r2 < L) {
+            const int flip = lane & 1;
+            ws.cpm[r2] = cand;
+            ws.cw[r2] = flip ? 1.f - ipar : ipar;
+            ws.cb[r2] = ipa;
+            ws.cp[r2] = ifl | (flip << j);
+        }
+        __syncwarp();
+        if (lane < L) {
+            spm = ws.cpm[lane];
+            spar = ws.cw[lane];
+            sparent = ws.cb[lane];
+            sfl = ws.cp[lane];
+        }
+        __syncwarp();
+    }
+    // beta = sign xor flips; the least reliable bit makes the parity even (:114-118)
+    const int parent = __shfl_sync(kFull, sparent, p);
+    const int fl = __shfl_sync(kFull, sfl, p);
+    const u32 psg = (sbal >> (parent * C::LPP)) & AM;
+    int b = (int)((psg >> u) & 1u);
+#pragma unroll
+    for (int j = 1; j <= TAU; j++)
+        if ((fl >> j) & 1) b ^= ws.sord[parent * 16 + j] == u;
+    const int tot = (__popc(psg) + __popc(fl)) & 1;
+    if (ws.sord[parent * 16] == u) b ^= tot;
+    if (lane < L) {
+        ws.pm[lane] = spm;
+        lin[lane] = (int8_t)sparent;
+    }
+    __syncwarp();
+    return act ? (u64)b : 0ull;
+}
+
 // ---------------------------------------------------- SPC node ----------
 // spc_decode_list (list_engine.py:68-119) on L paths of size n = 2^SS.
 template <int R, int MM, int L, int SS>
 __device__ __forceinline__ u64 spc_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / L>::V], int8_t* lin) {
+    if constexpr (Lv<SS, 32 / L>::V == 1 && (1 << SS) <= 16) return spc_node_v1<R, MM, L, SS>(cx, x[0], lin);
     using C = Cfg<R, MM, L>;
     using LV = Lv<SS, C::LPP>;
     constexpr int n = LV::n, V = LV::V;
