@@ -46,7 +46,8 @@ enum {
                                   throughput kernel (whose LM / llr_abs summation orders differ) */
     RMFHT_NO_LOCKSTEP = 16,    /* throughput kernel: no barrier between rounds of work items */
     RMFHT_LOCKSTEP_4 = 32,     /* ... barrier per group of 4 warps instead of the whole CTA */
-    RMFHT_LOCKSTEP_8 = 64      /* ... per group of 8 warps */
+    RMFHT_LOCKSTEP_8 = 64,     /* ... per group of 8 warps */
+    RMFHT_GENERIC = 128        /* use the generic runtime-shaped kernel even if a specialisation exists */
 };
 
 enum {
@@ -120,7 +121,8 @@ int rmfht_decode_launch_diag(const rmfht_plan *plan, const void *d_llr, const ui
 int rmfht_plan_launches_per_call(const rmfht_plan *plan);
 
 /* Which kernel the plan runs: 1 = reference-order (rmfht_kernels.cuh),
- * 2 = float32 throughput kernel (rmfht_fast.cuh); 0 for a NULL plan. */
+ * 2 = float32 throughput kernel (rmfht_fast.cuh), 3 = generic runtime-shaped
+ * kernel (rmfht_generic.cuh, reference order); 0 for a NULL plan. */
 int rmfht_plan_kernel(const rmfht_plan *plan);
 
 const char *rmfht_last_error(void);

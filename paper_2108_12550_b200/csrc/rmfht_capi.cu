@@ -30,10 +30,16 @@ int bind_any(rmfht_plan* p) {
     static const Binder f64[] = {rmfht_bind_double_0, rmfht_bind_double_1, rmfht_bind_double_2,
                                  rmfht_bind_double_3};
     const Binder* tab = p->dtype == RMFHT_F64 ? f64 : f32;
+    if (p->force_generic) {
+        if (rmfht_bind_generic(p) == 0) return 0;
+        return fail(RMFHT_EUNSUPPORTED, "shape outside the generic kernel's limits (m <= 10, L <= 16)");
+    }
     for (int c = 0; c < RMFHT_NCHUNKS; c++)
         if (tab[c](p) == 0) return 0;
+    if (rmfht_bind_generic(p) == 0) return 0;
     char buf[160];
-    snprintf(buf, sizeof buf, "no kernel compiled for RM(%d,%d) L=%d", p->r, p->m, p->L);
+    snprintf(buf, sizeof buf, "RM(%d,%d) L=%d is outside the compiled shapes and the generic kernel's limits "
+             "(m <= 10, L <= 16, workspace <= 220 KB)", p->r, p->m, p->L);
     return fail(RMFHT_EUNSUPPORTED, buf);
 }
 
@@ -121,6 +127,7 @@ int rmfht_plan_create(int r, int m, int L, int M, int flags, int dtype, rmfht_pl
     p->tie_fix = dtype == RMFHT_F32 ? 1 : 0;
     p->fast = (dtype == RMFHT_F32 && !(flags & RMFHT_REFERENCE_ORDER)) ? 1 : 0;
     p->lockstep = (flags & RMFHT_NO_LOCKSTEP) ? 0 : 16;
+    p->force_generic = (flags & RMFHT_GENERIC) ? 1 : 0;
     if (flags & RMFHT_LOCKSTEP_4) p->lockstep = 4;
     if (flags & RMFHT_LOCKSTEP_8) p->lockstep = 8;
     if (flags & RMFHT_TIE_FIX) p->tie_fix = 1;
@@ -155,7 +162,7 @@ int rmfht_plan_record_u16(const rmfht_plan* p) { return p ? 2 * p->m + 2 : fail(
 
 int rmfht_plan_launches_per_call(const rmfht_plan* p) { return p ? (p->fast ? 2 : 1) : 0; }  // + 1 when sampled
 
-int rmfht_plan_kernel(const rmfht_plan* p) { return p ? (p->fast ? 2 : 1) : 0; }
+int rmfht_plan_kernel(const rmfht_plan* p) { return p ? (p->fast ? 2 : (p->generic ? 3 : 1)) : 0; }
 
 int rmfht_expand_maps(const rmfht_plan* p, const uint16_t* raw, uint16_t* rec, long long count) {
     if (!p) return fail(RMFHT_EVALUE, "plan is NULL");

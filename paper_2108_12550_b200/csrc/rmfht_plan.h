@@ -18,6 +18,8 @@ struct rmfht_plan {
     int r, m, L, M, perms, tie_fix, dtype;
     int lockstep = 16;  // throughput kernel: warps per lock-step group (0 = none)
     int fast;  // float32 throughput kernel (rmfht_fast.cuh) instead of the reference-order one
+    int generic = 0;  // runtime-shaped interpreter kernel (rmfht_generic.cuh)
+    int force_generic = 0;
     int S, nwarps, grid;
     size_t smem;
     std::vector<int> sizes;
@@ -59,3 +61,4 @@ int fail(int code, const std::string& msg);
     int rmfht_bind_##T##_3(rmfht_plan* p);
 RMFHT_DECL_BINDERS(float)
 RMFHT_DECL_BINDERS(double)
+int rmfht_bind_generic(rmfht_plan* p);

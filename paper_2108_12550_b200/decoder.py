@@ -43,7 +43,7 @@ class Plan:
 
     def __init__(self, r: int, m: int, L: int, M: int = 1, permutations: bool = True,
                  dtype: str = "f32", tie_fix: bool | None = None, reference_order: bool = False,
-                 lockstep: int = 16):
+                 lockstep: int = 16, generic: bool = False):
         build_code(r, m)
         if L < 1 or M < 1:
             raise ConfigurationError("L, M and P must all be >= 1")
@@ -65,6 +65,8 @@ class Plan:
             flags |= _native.RMFHT_LOCKSTEP_4
         elif lockstep == 8:
             flags |= _native.RMFHT_LOCKSTEP_8
+        if generic:
+            flags |= _native.RMFHT_GENERIC
         lib = _native.lib()
         h = ctypes.c_void_p()
         _check(lib.rmfht_plan_create(r, m, L, M, flags,

@@ -35,7 +35,7 @@ def _create(r, m, L, M, flags=1, dtype=0):
 
 
 @pytest.mark.parametrize("r,m,L,M,code", [(0, 5, 1, 1, -1), (5, 5, 1, 1, -1), (2, 15, 1, 1, -1),
-                                          (2, 9, 0, 1, -1), (2, 9, 4, 0, -1), (2, 9, 3, 5, -3)])
+                                          (2, 9, 0, 1, -1), (2, 9, 4, 0, -1), (2, 12, 4, 5, -3)])
 def test_plan_create_errors(r, m, L, M, code):
     rc, h = _create(r, m, L, M)
     assert rc == code and not h.value
@@ -72,4 +72,17 @@ def test_expand_maps_matches_oracle(oracle_mod):
     raw[1, 2, 5, :] = 0
     assert lib.rmfht_expand_maps(h, raw.ctypes.data, rec.ctypes.data, raw.size // (m + 1)) == -2
     assert "invertible" in _native.last_error()
+    lib.rmfht_plan_destroy(h)
+
+
+def test_uncompiled_shape_binds_generic_kernel():
+    lib = _native.lib()
+    rc, h = _create(2, 9, 3, 5)
+    assert rc == 0 and lib.rmfht_plan_kernel(h) == 3
+    lib.rmfht_plan_destroy(h)
+    rc, h = _create(2, 9, 4, 20)
+    assert rc == 0 and lib.rmfht_plan_kernel(h) == 2
+    lib.rmfht_plan_destroy(h)
+    rc, h = _create(2, 9, 4, 20, 1, 1)
+    assert rc == 0 and lib.rmfht_plan_kernel(h) == 1
     lib.rmfht_plan_destroy(h)
