@@ -37,10 +37,32 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# BASELINE.json configurations: name -> (r, m, L, M, permutations, Eb/N0, frames per step)
+CONFIGS = {
+    "rm29_L4_M20": (2, 9, 4, 20, True, 2.5, 16384),   # headline
+    "rm27_L2_M4": (2, 7, 2, 4, True, 2.0, 262144),
+    "rm37_L8_M32": (3, 7, 8, 32, True, 4.0, 16384),
+    "rm29_L1_M512": (2, 9, 1, 512, True, 3.0, 1024),
+    "rm25_fhtfsc": (2, 5, 1, 1, False, 3.0, 1048576),
+}
 R, M_VARS, L, M = 2, 9, 4, 20
+PERMS = True
 EBN0 = 2.5
 WORKLOAD = "RM(2,9) p-FHT-FSCL L=4 M=20 (decoder 0 = identity), Eb/N0 2.5 dB"
 METRIC = "decoded frames/s, RM(2,9) M=20 L=4, 1 B200; % of roofline; vs host CPU"
+
+
+def select_config(name):
+    global R, M_VARS, L, M, PERMS, EBN0, WORKLOAD
+    r, m, l, mm, perms, ebn0, frames = CONFIGS[name]
+    R, M_VARS, L, M, PERMS, EBN0 = r, m, l, mm, perms, ebn0
+    algo = "p-FHT-FSCL" if perms else ("FHT-FSC" if l == 1 else "FHT-FSCL")
+    WORKLOAD = (f"RM({r},{m}) {algo} L={l} M={mm}" + (" (decoder 0 = identity)" if perms else "") +
+                f", Eb/N0 {ebn0} dB")
+    global METRIC
+    if name != "rm29_L4_M20":
+        METRIC = f"decoded frames/s, RM({r},{m}) {algo} L={l} M={mm}, 1 B200"
+    return frames
 
 
 def _peaks():
@@ -107,28 +129,49 @@ def make_inputs(plan, spec, B, seed):
     from paper_2108_12550_b200.channel_model import synthetic_frames
 
     x, llr = synthetic_frames(spec, EBN0, B, seed)
-    _, recs = plan.sample(B, seed, identity_root=True, want_raw=False)
+    recs = None
+    if plan.permutations:
+        _, recs = plan.sample(B, seed, identity_root=True, want_raw=False)
     return x, llr, recs
 
 
-def cpu_baseline(seconds: float = 12.0):
-    """Oracle port (float64 restatement) on all host cores over a bounded sample."""
-    from oracle import oracle
+def _cpu_batches(B, count, seed0):
     from paper_2108_12550_b200.channel_model import synthetic_frames
     from paper_2108_12550_b200.plan import map_sizes
     from paper_2108_12550_b200.automorphism import random_raw_table
     from paper_2108_12550_b200.rm_core import build_code
 
     spec = build_code(R, M_VARS)
+    out = []
+    for s in range(count):
+        _, llr = synthetic_frames(spec, EBN0, B, seed0 + s)
+        raw = (random_raw_table(np.random.default_rng(seed0 + s), (B, M), map_sizes(R, M_VARS, L), M_VARS,
+                                identity_root=L) if PERMS else None)
+        out.append((llr, raw))
+    return out
+
+
+def _cpu_decode(llr, raw, cores):
+    from oracle import oracle
+    oracle.decode(R, M_VARS, L, M if PERMS else 1, llr, raw, perms=PERMS, dtype=np.float64, nthreads=cores,
+                  want_attempts=False)
+
+
+def cpu_baseline(seconds: float = 12.0):
+    """Oracle port (float64 restatement) on all host cores over a bounded sample."""
     cores = os.cpu_count() or 1
     done, t_used, frames = 0, 0.0, 0
     B = 16 * cores
+    # calibrate the batch so one call is ~1/8 of the budget
+    (llr, raw), = _cpu_batches(B, 1, 1000)
+    t0 = time.perf_counter()
+    _cpu_decode(llr, raw, cores)
+    dt = time.perf_counter() - t0
+    B = max(B, int(B * (seconds / 8) / max(dt, 1e-3)))
     while t_used < seconds and done < 64:
-        _, llr = synthetic_frames(spec, EBN0, B, 1000 + done)
-        raw = random_raw_table(np.random.default_rng(done), (B, M), map_sizes(R, M_VARS, L), M_VARS,
-                               identity_root=L)
+        (llr, raw), = _cpu_batches(B, 1, 1001 + done)
         t0 = time.perf_counter()
-        oracle.decode(R, M_VARS, L, M, llr, raw, dtype=np.float64, nthreads=cores, want_attempts=False)
+        _cpu_decode(llr, raw, cores)
         t_used += time.perf_counter() - t0
         frames += B
         done += 1
@@ -141,25 +184,18 @@ def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return
-    from oracle import oracle
-    from paper_2108_12550_b200.channel_model import synthetic_frames
-    from paper_2108_12550_b200.plan import map_sizes
-    from paper_2108_12550_b200.automorphism import random_raw_table
-    from paper_2108_12550_b200.rm_core import build_code
-
-    spec = build_code(R, M_VARS)
     cores = os.cpu_count() or 1
-    B = 16 * cores
-    batches = []
-    for s in range(args.steps + args.warmup):
-        _, llr = synthetic_frames(spec, EBN0, B, 500 + s)
-        raw = random_raw_table(np.random.default_rng(s), (B, M), map_sizes(R, M_VARS, L), M_VARS, identity_root=L)
-        batches.append((llr, raw))
+    # bounded per-step sample: ~1.5 s of CPU work per step
+    (llr, raw), = _cpu_batches(16 * cores, 1, 400)
+    t0 = time.perf_counter()
+    _cpu_decode(llr, raw, cores)
+    B = max(16 * cores, int(16 * cores * 1.5 / max(time.perf_counter() - t0, 1e-3)))
+    batches = _cpu_batches(B, args.steps + args.warmup, 500)
     for llr, raw in batches[:args.warmup]:
-        oracle.decode(R, M_VARS, L, M, llr, raw, dtype=np.float64, nthreads=cores, want_attempts=False)
+        _cpu_decode(llr, raw, cores)
     t0 = time.perf_counter()
     for llr, raw in batches[args.warmup:]:
-        oracle.decode(R, M_VARS, L, M, llr, raw, dtype=np.float64, nthreads=cores, want_attempts=False)
+        _cpu_decode(llr, raw, cores)
     dt = time.perf_counter() - t0
     v = B * args.steps / dt
     line = {"metric": METRIC, "value": v, "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
@@ -187,12 +223,12 @@ def run_gpu(args):
     from paper_2108_12550_b200.rm_core import build_code
 
     spec = build_code(R, M_VARS)
-    plan = Plan(R, M_VARS, L, M, True, "f32", lockstep=0 if args.no_lockstep else args.lockstep)
+    plan = Plan(R, M_VARS, L, M, PERMS, "f32", lockstep=0 if args.no_lockstep else args.lockstep)
     B = args.frames
     x, llr, recs = make_inputs(plan, spec, B, seed=1 + rank)  # host table: decode-only timing
     dev = torch.device("cuda", local)
     d_llr = torch.from_numpy(llr).to(dev)
-    d_rec = torch.from_numpy(recs.view(np.int16)).to(dev)
+    d_rec = torch.from_numpy(recs.view(np.int16)).to(dev) if recs is not None else None
     out = plan.alloc_outputs(B, dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -272,12 +308,12 @@ def run_gpu(args):
     if rank == 0:
         hbm, sm_mhz, src = _peaks()
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        ops = complexity_ops(R, M_VARS, L, M, True, include_perm=True)
+        ops = complexity_ops(R, M_VARS, L, M, PERMS, include_perm=True, fsc=not PERMS and L == 1)
         peak_gops = sms * 128 * sm_mhz * 1e6 / 1e9
         per_gpu = value / ws
         ach_gops = ops * per_gpu / 1e9
         bytes_frame = 4 * spec.N + spec.N // 8
-        rec_bytes_frame = 2 * M * plan.S * plan.rec_u16 * 2  # table written by the sampler, read by the decoder
+        rec_bytes_frame = 2 * plan.M * plan.S * plan.rec_u16 * 2  # table written by the sampler, read by the decoder
         clk = clk.summary()
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
@@ -314,7 +350,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--frames", type=int, default=16384)
+    ap.add_argument("--frames", type=int, default=None)
+    ap.add_argument("--config", default="rm29_L4_M20", choices=sorted(CONFIGS),
+                    help="BASELINE.json configuration (default: the headline)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-lockstep", action="store_true", help="throughput kernel without per-round barriers")
@@ -323,6 +361,9 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    frames = select_config(args.config)
+    if args.frames is None:
+        args.frames = frames
     if args.impl == "reference":
         run_reference(args)
     else:
