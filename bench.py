@@ -320,7 +320,7 @@ def run_gpu(args):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": WORKLOAD, "frames_per_step": B, "parallelism": f"replicas{ws}",
-                       "l2": f"inputs {(llr.nbytes + recs.nbytes) / 2**20:.0f} MiB/step > 126 MB L2, no flush",
+                       "l2": f"inputs {(llr.nbytes + (recs.nbytes if recs is not None else 0)) / 2**20:.0f} MiB/step > 126 MB L2, no flush",
                        "fer_check": fer_warm},
             "e2e": {"value": e2e, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps": e_steps},

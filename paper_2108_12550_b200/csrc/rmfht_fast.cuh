@@ -99,6 +99,8 @@ struct Lv {
 template <int R, int MM, int L>
 struct alignas(16) WS2 {
     using C = Cfg<R, MM, L>;
+    static constexpr int RECW = (C::S > 0 ? C::S : 1) * (2 * MM + 2);  // uint16 per item's map records
+    alignas(16) uint16_t recs[2][(RECW + 7) & ~7];  // double-buffered (cp.async prefetch)
     float lmp[2 * L][32];       // LM lane partials per trial
     MapS maps[C::S > 0 ? C::S : 1];
     MapS comp[L];     // composite map of each root path (root perm-ext winners)
@@ -198,6 +200,17 @@ struct RootIdx {
 __device__ __forceinline__ float lds_byte(const float* base, u32 byteoff) {
     return *reinterpret_cast<const float*>(reinterpret_cast<const char*>(base) + byteoff);
 }
+// asynchronous global -> shared copies (LDGSTS), used to prefetch the next
+// work item's LLRs and map records while the current item decodes
+__device__ __forceinline__ void cp_async16(u32 saddr, const void* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async4(u32 saddr, const void* g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // load from a 32-bit shared-window address (the gather tables carry the base)
 __device__ __forceinline__ float lds_addr(u32 saddr) {
     float v;
@@ -1160,28 +1173,44 @@ __global__ void __launch_bounds__(512, 1) decode_kernel2(rmfht::Params<float> pr
     const u32 raw_saddr = (u32)__cvta_generic_to_shared(smem_raw);
     const u32 pad = ((raw_saddr + 2047u) & ~2047u) - raw_saddr;
     constexpr u32 ASTRIDE = ((u32)N * 4u + 2047u) & ~2047u;
-    float* alpha_w = reinterpret_cast<float*>(smem_raw + pad + (size_t)warp * ASTRIDE);
-    WS* wsarr = reinterpret_cast<WS*>(smem_raw + pad + (size_t)nwarps * ASTRIDE);
+    // the warp's two LLR buffers are adjacent: buffer b at alpha0 + b * ASTRIDE bytes
+    float* const alpha0 = reinterpret_cast<float*>(smem_raw + pad + (size_t)(2 * warp) * ASTRIDE);
+    auto alpha_buf = [&](int b) { return reinterpret_cast<float*>(reinterpret_cast<char*>(alpha0) + b * ASTRIDE); };
+    WS* wsarr = reinterpret_cast<WS*>(smem_raw + pad + (size_t)(2 * nwarps) * ASTRIDE);
     WS& ws = wsarr[warp];
-    Ctx2<R, MM, L> cx{ws, alpha_w, {}, lane, lane / C::LPP, lane % C::LPP,
-                      (u32)__cvta_generic_to_shared(alpha_w)};
+    Ctx2<R, MM, L> cx{ws, alpha0, {}, lane, lane / C::LPP, lane % C::LPP, (u32)__cvta_generic_to_shared(alpha0)};
     constexpr bool ROOT_INTERNAL = !(R == 1 || R == MM - 1);
     const long long items = prm.B * (long long)prm.M;
-    long long cur_f = -1;
-    for (long long base = (long long)blockIdx.x * nwarps; base < items; base += (long long)gridDim.x * nwarps) {
+    const long long stride = (long long)gridDim.x * nwarps;
+    // prefetch one work item's LLRs and map records into buffer `buf`
+    auto prefetch = [&](long long it, int buf) {
+        if (it >= items) return;
+        const long long f = it / prm.M;
+        const u32 asa = (u32)__cvta_generic_to_shared(alpha_buf(buf));
+        const char* ga = reinterpret_cast<const char*>(prm.llr + f * N);
+        for (int i = lane; i < N / 4; i += 32) cp_async16(asa + 16u * i, ga + 16 * i);
+        const u32 rsa = (u32)__cvta_generic_to_shared(ws.recs[buf]);
+        const char* gr = reinterpret_cast<const char*>(prm.maps + (size_t)it * S * REC);
+        for (int i = lane; i < WS::RECW / 2; i += 32) cp_async4(rsa + 4u * i, gr + 4 * i);
+        cp_async_commit();
+    };
+    int cur = 0;
+    prefetch((long long)blockIdx.x * nwarps + warp, 0);
+    for (long long base = (long long)blockIdx.x * nwarps; base < items; base += stride) {
         const long long item = base + warp;
         if (item < items) {
             const long long f = item / prm.M;
             const int a = (int)(item % prm.M);
-            if (f != cur_f) {
-                const float4* src4 = reinterpret_cast<const float4*>(prm.llr + f * N);
-                for (int i = lane; i < N / 4; i += 32) reinterpret_cast<float4*>(alpha_w)[i] = src4[i];
-                __syncwarp();
+            cp_async_wait_all();
+            __syncwarp();
+            prefetch(item + stride, cur ^ 1);  // overlaps with this item's decode
+            float* alpha_w = alpha_buf(cur);
+            cx.alpha = alpha_w;
+            cx.alpha_saddr = (u32)__cvta_generic_to_shared(alpha_w);
 #pragma unroll
-                for (int s = 0; s < C::NS; s++) cx.ach[s] = alpha_w[lane + 32 * s];
-                cur_f = f;
-            }
-            const uint16_t* recs = prm.maps + (size_t)item * S * REC;
+            for (int s = 0; s < C::NS; s++) cx.ach[s] = alpha_w[lane + 32 * s];
+            (void)f;
+            const uint16_t* recs = ws.recs[cur];
             for (int s = lane; s < S; s += 32) {
                 const int mn = s < L ? MM : MM - (s - L) / (2 * L);
                 rmfht::load_map(ws.maps[s], recs + (size_t)s * REC, MM, mn);
@@ -1224,6 +1253,7 @@ __global__ void __launch_bounds__(512, 1) decode_kernel2(rmfht::Params<float> pr
             }
             if (cx.p == best) bitsout[(size_t)item * C::LPP + cx.u] = bits;
             __syncwarp();
+            cur ^= 1;
         }
         // lock-step rounds: warps share the instruction stream (named barrier per group)
         const int grp = (prm.tie_fix >> 8) & 0xff;  // warps per lock-step group, 0 = none
@@ -1309,8 +1339,8 @@ __global__ void __launch_bounds__(256) reduce_kernel2(rmfht::Params<float> prm, 
 
 template <int R, int MM, int L>
 constexpr size_t smem_bytes2(int nwarps) {
-    // 2 KB alignment pad + per-warp LLR copies + per-warp scratch
-    return 2048 + ((size_t(1 << MM) * 4 + 2047) & ~size_t(2047)) * size_t(nwarps) +
+    // 2 KB alignment pad + two per-warp LLR copies (prefetch) + per-warp scratch
+    return 2048 + ((size_t(1 << MM) * 4 + 2047) & ~size_t(2047)) * size_t(2 * nwarps) +
            sizeof(WS2<R, MM, L>) * size_t(nwarps);
 }
 

@@ -10,10 +10,13 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 rows = list(csv.reader(out.splitlines()))
 h = rows[1]
 iA, iS, iE = h.index("Address"), h.index("Source"), h.index("Instructions Executed")
+iW = h.index("Warp Stall Sampling (All Samples)")
+metric = os.environ.get("NCU_LINES_METRIC", "exec")
 execs = []
 for r in rows[2:]:
     if len(r) > iE and r[iA].startswith("0x"):
-        execs.append((int(r[iA], 16), r[iS].strip(), int(r[iE] or 0)))
+        val = int(r[iE] or 0) if metric == "exec" else int(r[iW] or 0)
+        execs.append((int(r[iA], 16), r[iS].strip(), val))
 base = execs[0][0]
 d = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=d, capture_output=True)
