@@ -1097,8 +1097,9 @@ __device__ __forceinline__ u64 node2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / 
 // Internal root (1 < r < m-1): the root vectors are never held; f (:100) and
 // g (:104) read them straight from the frame LLRs through each path's
 // composite map, g after the left child's lineage (:102) re-selects the maps.
-template <int R, int MM, int L>
-__device__ __forceinline__ u64 root_node(Ctx2<R, MM, L>& cx, int8_t* lin) {
+// `alpha_dead` runs once the frame LLRs have been read for the last time.
+template <int R, int MM, int L, typename F>
+__device__ __forceinline__ u64 root_node(Ctx2<R, MM, L>& cx, int8_t* lin, F&& alpha_dead) {
     using C = Cfg<R, MM, L>;
     using LV = Lv<MM, C::LPP>;
     using LC = Lv<MM - 1, C::LPP>;
@@ -1128,6 +1129,7 @@ __device__ __forceinline__ u64 root_node(Ctx2<R, MM, L>& cx, int8_t* lin) {
                 ga[k] = lds_addr(ri.off(k));
                 gb[k] = lds_addr(ri.off(k + VC));
             }
+            alpha_dead();
             g_fht_child<R, MM, L, MM - 1>(cx, p, ga, gb, xr);
         } else {
 #pragma unroll
@@ -1135,6 +1137,7 @@ __device__ __forceinline__ u64 root_node(Ctx2<R, MM, L>& cx, int8_t* lin) {
                 const float sg = ((bl >> k) & 1ull) ? -1.f : 1.f;
                 xr[k] = __fmaf_rn(sg, lds_addr(ri.off(k)), lds_addr(ri.off(k + VC)));
             }
+            alpha_dead();
         }
     }
     const u64 br = node2<R, MM, L, R, MM - 1, false>(cx, xr, l2);
@@ -1173,29 +1176,35 @@ __global__ void __launch_bounds__(512, 1) decode_kernel2(rmfht::Params<float> pr
     const u32 raw_saddr = (u32)__cvta_generic_to_shared(smem_raw);
     const u32 pad = ((raw_saddr + 2047u) & ~2047u) - raw_saddr;
     constexpr u32 ASTRIDE = ((u32)N * 4u + 2047u) & ~2047u;
-    // the warp's two LLR buffers are adjacent: buffer b at alpha0 + b * ASTRIDE bytes
-    float* const alpha0 = reinterpret_cast<float*>(smem_raw + pad + (size_t)(2 * warp) * ASTRIDE);
-    auto alpha_buf = [&](int b) { return reinterpret_cast<float*>(reinterpret_cast<char*>(alpha0) + b * ASTRIDE); };
-    WS* wsarr = reinterpret_cast<WS*>(smem_raw + pad + (size_t)(2 * nwarps) * ASTRIDE);
+    float* const alpha_w = reinterpret_cast<float*>(smem_raw + pad + (size_t)warp * ASTRIDE);
+    WS* wsarr = reinterpret_cast<WS*>(smem_raw + pad + (size_t)nwarps * ASTRIDE);
     WS& ws = wsarr[warp];
-    Ctx2<R, MM, L> cx{ws, alpha0, {}, lane, lane / C::LPP, lane % C::LPP, (u32)__cvta_generic_to_shared(alpha0)};
+    const u32 asa = (u32)__cvta_generic_to_shared(alpha_w);
+    Ctx2<R, MM, L> cx{ws, alpha_w, {}, lane, lane / C::LPP, lane % C::LPP, asa};
     constexpr bool ROOT_INTERNAL = !(R == 1 || R == MM - 1);
     const long long items = prm.B * (long long)prm.M;
     const long long stride = (long long)gridDim.x * nwarps;
-    // prefetch one work item's LLRs and map records into buffer `buf`
-    auto prefetch = [&](long long it, int buf) {
+    // Prefetch (LDGSTS) of the warp's next work item: its map records into the
+    // idle half of ws.recs at item start, its LLRs into the single LLR buffer
+    // as soon as the current item has read the frame LLRs for the last time
+    // (after the root's g, i.e. before the right half of the tree).
+    auto prefetch_recs = [&](long long it, int buf) {
         if (it >= items) return;
-        const long long f = it / prm.M;
-        const u32 asa = (u32)__cvta_generic_to_shared(alpha_buf(buf));
-        const char* ga = reinterpret_cast<const char*>(prm.llr + f * N);
-        for (int i = lane; i < N / 4; i += 32) cp_async16(asa + 16u * i, ga + 16 * i);
         const u32 rsa = (u32)__cvta_generic_to_shared(ws.recs[buf]);
         const char* gr = reinterpret_cast<const char*>(prm.maps + (size_t)it * S * REC);
         for (int i = lane; i < WS::RECW / 2; i += 32) cp_async4(rsa + 4u * i, gr + 4 * i);
         cp_async_commit();
     };
+    auto prefetch_alpha = [&](long long it) {
+        if (it >= items) return;
+        __syncwarp();  // every lane is past its last read of the current LLRs
+        const char* ga = reinterpret_cast<const char*>(prm.llr + (it / prm.M) * N);
+        for (int i = lane; i < N / 4; i += 32) cp_async16(asa + 16u * i, ga + 16 * i);
+        cp_async_commit();
+    };
     int cur = 0;
-    prefetch((long long)blockIdx.x * nwarps + warp, 0);
+    prefetch_recs((long long)blockIdx.x * nwarps + warp, 0);
+    prefetch_alpha((long long)blockIdx.x * nwarps + warp);
     for (long long base = (long long)blockIdx.x * nwarps; base < items; base += stride) {
         const long long item = base + warp;
         if (item < items) {
@@ -1203,10 +1212,7 @@ __global__ void __launch_bounds__(512, 1) decode_kernel2(rmfht::Params<float> pr
             const int a = (int)(item % prm.M);
             cp_async_wait_all();
             __syncwarp();
-            prefetch(item + stride, cur ^ 1);  // overlaps with this item's decode
-            float* alpha_w = alpha_buf(cur);
-            cx.alpha = alpha_w;
-            cx.alpha_saddr = (u32)__cvta_generic_to_shared(alpha_w);
+            prefetch_recs(item + stride, cur ^ 1);
 #pragma unroll
             for (int s = 0; s < C::NS; s++) cx.ach[s] = alpha_w[lane + 32 * s];
             (void)f;
@@ -1228,13 +1234,14 @@ __global__ void __launch_bounds__(512, 1) decode_kernel2(rmfht::Params<float> pr
             u64 bits;
             if constexpr (ROOT_INTERNAL) perm_ext_root2(cx);
             if constexpr (ROOT_INTERNAL && Lv<MM - 1, C::LPP>::full) {
-                bits = root_node(cx, rlin);
+                bits = root_node(cx, rlin, [&] { prefetch_alpha(item + stride); });
             } else {
                 float x[V];
                 RootIdx<MM, C::LPP, V> ri;
                 ri.build(ws.comp[cx.p], cx.u, cx.alpha_saddr);
 #pragma unroll
                 for (int k = 0; k < V; k++) x[k] = lds_addr(ri.off(k));
+                prefetch_alpha(item + stride);
                 bits = node2<R, MM, L, R, MM, true>(cx, x, rlin);
             }
             // best path: first minimum (:152)
@@ -1339,8 +1346,8 @@ __global__ void __launch_bounds__(256) reduce_kernel2(rmfht::Params<float> prm, 
 
 template <int R, int MM, int L>
 constexpr size_t smem_bytes2(int nwarps) {
-    // 2 KB alignment pad + two per-warp LLR copies (prefetch) + per-warp scratch
-    return 2048 + ((size_t(1 << MM) * 4 + 2047) & ~size_t(2047)) * size_t(2 * nwarps) +
+    // 2 KB alignment pad + per-warp LLR copy + per-warp scratch
+    return 2048 + ((size_t(1 << MM) * 4 + 2047) & ~size_t(2047)) * size_t(nwarps) +
            sizeof(WS2<R, MM, L>) * size_t(nwarps);
 }
 
