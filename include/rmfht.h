@@ -78,8 +78,9 @@ int rmfht_plan_record_u16(const rmfht_plan *plan); /* 2m+2 */
 int rmfht_expand_maps(const rmfht_plan *plan, const uint16_t *raw, uint16_t *rec, long long count);
 
 /* Host: sample the permutation table of frames frame0 .. frame0+B-1 —
- * uniform (A, b) in GL(m_node, 2) x F_2^m_node per slot by rejection on
- * random row masks (the reference's rule, automorphism.py:127-161), from a
+ * uniform (A, b) in GL(m_node, 2) x F_2^m_node per slot (the reference
+ * sampler's distribution, automorphism.py:127-161; A drawn column by column,
+ * each uniform outside the span of the previous ones), from a
  * counter-based stream keyed by (seed, frame, attempt, slot), so a frame's
  * maps do not depend on the batch it is drawn in.  identity_root != 0 makes
  * attempt 0's L root maps the identity ("decoder 0 = identity").  Writes raw

@@ -52,53 +52,65 @@ struct SampleArgs {
     signed char sizes[128];
 };
 
-// one warp per (frame, attempt): the classes of its slots are filled with
-// candidates tested 32 at a time (ballot keeps the candidate order)
-template <int MN>
-__device__ __forceinline__ void fill_class_dev(const SampleArgs& a, long long f, int at, int c, int s0, int cnt,
-                                               uint16_t* rec_item) {
-    const int lane = threadIdx.x & 31;
-    int filled = 0;
-    for (long long base = 0; filled < cnt; base += 32) {
-        unsigned rows[MN], inv[MN], b;
-        const bool ok = rmfht_maps::candidate<MN>(rmfht_maps::cand_key(a.seed, f, at, c, base + lane), rows, inv, b);
-        const unsigned bal = __ballot_sync(0xffffffffu, ok);
-        const int rank = __popc(bal & ((1u << lane) - 1u));
-        if (ok && filled + rank < cnt) {
-            uint16_t r[2 * 14 + 2];
-            rmfht_maps::write_map<MN>(rows, inv, b, a.m, nullptr, r);
-            uint16_t* o = rec_item + (size_t)(s0 + filled + rank) * (2 * a.m + 2);
-            for (int k = 0; k < 2 * a.m + 2; k++) o[k] = r[k];
-        }
-        filled += __popc(bal);
+// one record (2MG+2 uint16 = MG+1 words) built in registers
+template <int MN, int MG>
+__device__ __forceinline__ void draw_store(uint64_t key, uint32_t* o) {
+    unsigned cols[MN], icols[MN], b;
+    rmfht_maps::draw_map<MN>(key, cols, icols, b);
+    // record halves: cols of A (MG), b, cols of A^-1 (MG), A^-1 b
+    unsigned h[2 * MG + 2];
+#pragma unroll
+    for (int k = 0; k < MG; k++) {
+        h[k] = k < MN ? cols[k < MN ? k : 0] : 0u;
+        h[MG + 1 + k] = k < MN ? icols[k < MN ? k : 0] : 0u;
     }
+    h[MG] = b;
+    h[2 * MG + 1] = rmfht_maps::inv_shift<MN>(icols, b);
+#pragma unroll
+    for (int w = 0; w <= MG; w++) o[w] = h[2 * w] | (h[2 * w + 1] << 16);
 }
 
+// slots below MG-2 variables (r >= 5)
+template <int MG>
+__device__ __noinline__ void draw_store_rt(uint64_t key, int mn, uint16_t* o) {
+    unsigned cols[16], icols[16], b;
+    rmfht_maps::draw_map_rt(key, mn, cols, icols, b);
+    unsigned cinv = 0;
+    for (int k = 0; k < MG; k++) {
+        o[k] = (uint16_t)(k < mn ? cols[k] : 0u);
+        o[MG + 1 + k] = (uint16_t)(k < mn ? icols[k] : 0u);
+        if (k < mn && ((b >> k) & 1u)) cinv ^= icols[k];
+    }
+    o[MG] = (uint16_t)b;
+    o[2 * MG + 1] = (uint16_t)cinv;
+}
+
+// One thread per (frame, attempt, slot); a warp takes one slot of 32
+// consecutive (frame, attempt) items, so its lanes draw maps of one size.
 template <int MG>
 __global__ void __launch_bounds__(256) sample_kernel(SampleArgs a, uint16_t* rec) {
     const long long items = a.B * (long long)a.M;
+    const long long groups = (items + 31) / 32;
     const int lane = threadIdx.x & 31;
-    for (long long item = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; item < items;
-         item += (long long)gridDim.x * blockDim.x / 32) {
+    const long long nwarps = (long long)gridDim.x * blockDim.x / 32;
+    for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; w < groups * a.S; w += nwarps) {
+        const int s = (int)(w % a.S);
+        const long long item = (w / a.S) * 32 + lane;
+        if (item >= items) continue;
         const long long f = a.frame0 + item / a.M;
         const int at = (int)(item % a.M);
-        uint16_t* rec_item = rec + (size_t)item * a.S * (2 * MG + 2);
-        int s = 0, c = 0;
-        while (s < a.S) {
-            const int mn = a.sizes[s];
-            int e = s;
-            while (e < a.S && a.sizes[e] == mn) e++;
-            int s0 = s;
-            if (a.identity_root && at == 0 && s == 0) {
-                for (int t = lane; t < a.L; t += 32) rmfht_maps::write_identity(mn, MG, nullptr, rec_item + (size_t)t * (2 * MG + 2));
-                s0 = a.L;
-            }
-            if (mn == MG) fill_class_dev<MG>(a, f, at, c, s0, e - s0, rec_item);
-            else if (mn == MG - 1 && MG > 1) fill_class_dev<(MG > 1 ? MG - 1 : 1)>(a, f, at, c, s0, e - s0, rec_item);
-            else if (mn == MG - 2 && MG > 2) fill_class_dev<(MG > 2 ? MG - 2 : 1)>(a, f, at, c, s0, e - s0, rec_item);
-            s = e;
-            c++;
+        uint16_t* o = rec + ((size_t)item * a.S + s) * (2 * MG + 2);
+        const int mn = a.sizes[s];
+        if (a.identity_root && at == 0 && s < a.L) {
+            rmfht_maps::write_identity(mn, MG, nullptr, o);
+            continue;
         }
+        const uint64_t key = rmfht_maps::slot_key(a.seed, f, at, s);
+        uint32_t* o32 = reinterpret_cast<uint32_t*>(o);
+        if (mn == MG) draw_store<MG, MG>(key, o32);
+        else if (mn == MG - 1 && MG > 1) draw_store<(MG > 1 ? MG - 1 : 1), MG>(key, o32);
+        else if (mn == MG - 2 && MG > 2) draw_store<(MG > 2 ? MG - 2 : 1), MG>(key, o32);
+        else draw_store_rt<MG>(key, mn, o);
     }
 }
 
@@ -193,21 +205,14 @@ int rmfht_sample_maps(const rmfht_plan* p, uint64_t seed, long long frame0, long
         const int at = (int)(item % M);
         uint16_t* raw_i = raw ? raw + (size_t)item * S * (mg + 1) : nullptr;
         uint16_t* rec_i = rec ? rec + (size_t)item * S * (2 * mg + 2) : nullptr;
-        int s = 0, c = 0;
-        while (s < S) {
+        for (int s = 0; s < S; s++) {
             const int mn = p->sizes[s];
-            int e = s;
-            while (e < S && p->sizes[e] == mn) e++;
-            int s0 = s;
-            if (identity_root && at == 0 && s == 0) {
-                for (int t = 0; t < p->L; t++)
-                    rmfht_maps::write_identity(mn, mg, raw_i ? raw_i + (size_t)t * (mg + 1) : nullptr,
-                                               rec_i ? rec_i + (size_t)t * (2 * mg + 2) : nullptr);
-                s0 = p->L;
-            }
-            rmfht_maps::fill_class_host_any(mn, seed, f, at, c, s0, e - s0, mg, raw_i, rec_i);
-            s = e;
-            c++;
+            uint16_t* raw_s = raw_i ? raw_i + (size_t)s * (mg + 1) : nullptr;
+            uint16_t* rec_s = rec_i ? rec_i + (size_t)s * (2 * mg + 2) : nullptr;
+            if (identity_root && at == 0 && s < p->L)
+                rmfht_maps::write_identity(mn, mg, raw_s, rec_s);
+            else
+                rmfht_maps::fill_slot_host_any(mn, rmfht_maps::slot_key(seed, f, at, s), mg, raw_s, rec_s);
         }
     }
     return 0;
@@ -229,7 +234,7 @@ int rmfht_sample_maps_device(const rmfht_plan* p, uint64_t seed, long long frame
     a.m = p->m;
     a.identity_root = identity_root;
     for (int s = 0; s < p->S; s++) a.sizes[s] = (signed char)p->sizes[s];
-    const long long warps = B * (long long)p->M;
+    const long long warps = (B * (long long)p->M + 31) / 32 * p->S;
     long long blocks = (warps * 32 + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -135,7 +135,7 @@ def test_zero_noise_round_trip():
     assert np.array_equal(o["cw"], x) and np.all(o["pm"] == 0)
 
 
-@pytest.mark.parametrize("r,m,L,M", [(2, 9, 4, 20), (3, 7, 8, 32), (2, 7, 2, 4)])
+@pytest.mark.parametrize("r,m,L,M", [(2, 9, 4, 20), (3, 7, 8, 32), (2, 7, 2, 4), (4, 9, 2, 3), (5, 8, 2, 3)])
 def test_device_sampler_matches_host(r, m, L, M):
     import torch
     from paper_2108_12550_b200.decoder import Plan

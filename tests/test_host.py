@@ -84,23 +84,37 @@ def test_counter_sampler_uniform_over_gl3():
     uniformly from F_2^3 — the reference's distribution (automorphism.py:127-161)."""
     from paper_2108_12550_b200.decoder import Plan
     from scipy.stats import chisquare
-    plan = Plan(2, 5, 4, 8, True, "f32")      # root maps are m=5; use the m=5 masks' low 3x3? no:
-    # use a dedicated small code: RM(1,4) consumes L maps of size 4 per attempt
-    plan = Plan(1, 4, 4, 64, True, "f32") if False else plan
-    raw, _ = plan.sample(2000, seed=3, identity_root=False)
-    A = raw[..., :5].reshape(-1, 5).astype(np.int64)
-    # project to GL(5,2)-uniformity checks: each row mask uniform over nonzero? use the
-    # pairing direction d = A^-1 e_4, which is uniform over the 31 nonzero vectors
-    from paper_2108_12550_b200.automorphism import AffineMap
-    ds = []
-    for row in A[:20000]:
-        p = AffineMap.from_masks(row, 0, 5)
-        ds.append(int(p.inv[16] ^ p.inv[0]))
-    counts = np.bincount(ds, minlength=32)[1:]
-    assert counts.sum() == 20000 and np.all(counts > 0)
+    plan = Plan(1, 3, 4, 8, True, "f32")       # RM(1,3): L root maps of 3 variables per attempt
+    assert plan.S == 4 and list(plan.sizes) == [3, 3, 3, 3]
+    raw, _ = plan.sample(420, seed=3, identity_root=False)
+    A = raw[..., :3].reshape(-1, 3).astype(np.int64)
+    assert aut.gf2_invertible_masks(A, 3).all()
+    code = A[:, 0] | (A[:, 1] << 3) | (A[:, 2] << 6)
+    uniq, counts = np.unique(code, return_counts=True)
+    assert len(uniq) == 168 and counts.sum() == 420 * 8 * 4
     assert chisquare(counts).pvalue > 1e-4
-    b = raw[..., 5].ravel()
-    assert chisquare(np.bincount(b, minlength=32)).pvalue > 1e-4
+    b = raw[..., 3].ravel()
+    assert chisquare(np.bincount(b, minlength=8)).pvalue > 1e-4
+    # A and b independent: contingency of (A[0,0], b)
+    from scipy.stats import chi2_contingency
+    joint = np.bincount(((A[:, 0] & 1) * 8 + b).astype(np.int64), minlength=16).reshape(2, 8)
+    assert chi2_contingency(joint).pvalue > 1e-4
+
+
+def test_counter_sampler_uniform_over_gl9_projection():
+    """For m = 9 (the headline's root maps), the image of a fixed nonzero
+    vector under A is uniform over the 511 nonzero vectors."""
+    from paper_2108_12550_b200.decoder import Plan
+    from scipy.stats import chisquare
+    plan = Plan(2, 9, 4, 20, True, "f32")
+    raw, _ = plan.sample(300, seed=11, identity_root=False)
+    A = raw[..., :9].reshape(-1, 9).astype(np.int64)
+    img = np.zeros(len(A), dtype=np.int64)
+    for r in range(9):  # A @ (1,0,...,0, 1): columns 0 and 8
+        img |= (((A[:, r] >> 0) ^ (A[:, r] >> 8)) & 1) << r
+    counts = np.bincount(img, minlength=512)
+    assert counts[0] == 0
+    assert chisquare(counts[1:]).pvalue > 1e-4
 
 
 def test_counter_sampler_batch_independent_and_identity_root():
