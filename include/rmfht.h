@@ -118,6 +118,23 @@ int rmfht_decode_launch_diag(const rmfht_plan *plan, const void *d_llr, const ui
                              uint32_t *d_cw, void *d_pm, int32_t *d_attempt, int32_t *d_path,
                              void *d_att_pm, uint32_t *d_att_cw, long long B, void *stream);
 
+/* On-device frames: B frames frame0 .. frame0+B-1 of SNR
+ * point `point` — uniform info bits of RM(r, m) (rm_core.py:182-186), polar
+ * transform (rm_core.py:102-118), BPSK + AWGN with standard deviation sigma
+ * by the inverse-CDF method, LLR = 2y/sigma^2 (channel_model.py:41-61; the
+ * per-frame pipeline of harness.py:103-107).  Counter-based streams keyed by
+ * (seed, point, frame).  Writes d_llr [B, 2^m] float32 and the transmitted
+ * codewords d_tx [B, max(1, 2^m/32)] bit-packed like d_cw. */
+int rmfht_gen_frames(int r, int m, uint64_t seed, long long point, long long frame0, long long B, double sigma,
+                     int zero_noise, float *d_llr, uint32_t *d_tx, void *stream);
+
+/* Error counting (harness.py:79-84,109-112): for each of B frames, if d_cw
+ * differs from d_tx, d_counts[0] += 1, and if also corr(cw) >= corr(tx),
+ * corr(c) = sum (1-2c) llr (top_decoders.py:231), d_counts[1] += 1
+ * (maximum-likelihood lower bound).  d_counts: 2 x uint64, accumulated. */
+int rmfht_count_errors(int m, const float *d_llr, const uint32_t *d_tx, const uint32_t *d_cw, long long B,
+                       unsigned long long *d_counts, void *stream);
+
 /* Kernel launches per rmfht_decode_launch call (for the bench's launch count). */
 int rmfht_plan_launches_per_call(const rmfht_plan *plan);
 

@@ -29,7 +29,7 @@ EXPORTS = [
     "rmfht_plan_map_sizes", "rmfht_plan_record_u16", "rmfht_expand_maps",
     "rmfht_decode_launch", "rmfht_decode_launch_diag", "rmfht_plan_launches_per_call",
     "rmfht_last_error", "rmfht_version", "rmfht_sample_maps", "rmfht_plan_kernel",
-    "rmfht_sample_maps_device", "rmfht_decode_launch_sampled",
+    "rmfht_sample_maps_device", "rmfht_decode_launch_sampled", "rmfht_gen_frames", "rmfht_count_errors",
 ]
 
 _lib = None
@@ -44,7 +44,8 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
     objdir = os.path.join(_HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     units = [("rmfht_capi", os.path.join(CSRC, "rmfht_capi.cu"), []),
-             ("rmfht_gen", os.path.join(CSRC, "rmfht_gen.cu"), [])]
+             ("rmfht_gen", os.path.join(CSRC, "rmfht_gen.cu"), []),
+             ("rmfht_chan", os.path.join(CSRC, "rmfht_chan.cu"), [])]
     for t in ("float", "double"):
         for c in range(4):
             units.append((f"rmfht_bind_{t}_{c}", os.path.join(CSRC, "rmfht_bind.cu"),
@@ -105,6 +106,10 @@ def lib():
     L.rmfht_sample_maps_device.restype = I
     L.rmfht_decode_launch_sampled.argtypes = [P, P, ctypes.c_uint64, LL, I, P, P, P, P, LL, P]
     L.rmfht_decode_launch_sampled.restype = I
+    L.rmfht_gen_frames.argtypes = [I, I, ctypes.c_uint64, LL, LL, LL, ctypes.c_double, I, P, P, P]
+    L.rmfht_gen_frames.restype = I
+    L.rmfht_count_errors.argtypes = [I, P, P, P, LL, P, P]
+    L.rmfht_count_errors.restype = I
     L.rmfht_last_error.argtypes = []
     L.rmfht_last_error.restype = ctypes.c_char_p
     L.rmfht_version.argtypes = []

@@ -86,3 +86,34 @@ def synthetic_frames(spec: CodeSpec, ebn0_db: float, B: int, seed: int, dtype=np
     x = polar_transform(u)
     y = (1.0 - 2.0 * x) + chan.sigma * rng.standard_normal((B, spec.N))
     return x, (2.0 * y / chan.sigma ** 2).astype(dtype)
+
+
+# ------------------------------------------------- on-device generation
+def gen_frames_device(spec: CodeSpec, chan: ChannelConfig, point: int, frame0: int, llr, tx,
+                      zero_noise: bool = False, stream=None) -> None:
+    """Frames frame0 .. frame0+B-1 of SNR point `point` generated on the GPU
+    (rmfht_gen_frames: uniform info bits, polar transform, BPSK + inverse-CDF
+    AWGN, float32 LLR = 2y/sigma^2).  `llr` float32 [B, N] and `tx` int32
+    [B, max(1, N/32)] are CUDA tensors; stream-ordered, no host sync."""
+    from . import _native
+    from .decoder import _check, _torch
+    torch = _torch()
+    st = stream if stream is not None else torch.cuda.current_stream()
+    B = llr.shape[0]
+    if tuple(llr.shape) != (B, spec.N) or llr.dtype != torch.float32 or tx.shape[0] != B:
+        raise ValueError("llr must be float32 [B, N] and tx int32 [B, words]")
+    _check(_native.lib().rmfht_gen_frames(spec.r, spec.m, chan.seed & ((1 << 64) - 1), point, frame0, B,
+                                          chan.sigma, int(zero_noise), llr.data_ptr(), tx.data_ptr(),
+                                          st.cuda_stream))
+
+
+def count_errors_device(spec: CodeSpec, llr, tx, cw, counts, stream=None) -> None:
+    """Accumulate [frame errors, ML-lower-bound errors] of decoded words `cw`
+    against transmitted `tx` into the int64[2] CUDA tensor `counts`
+    (harness.py:79-84,109-112)."""
+    from . import _native
+    from .decoder import _check, _torch
+    torch = _torch()
+    st = stream if stream is not None else torch.cuda.current_stream()
+    _check(_native.lib().rmfht_count_errors(spec.m, llr.data_ptr(), tx.data_ptr(), cw.data_ptr(), llr.shape[0],
+                                            counts.data_ptr(), st.cuda_stream))

@@ -1208,14 +1208,11 @@ __global__ void __launch_bounds__(512, 1) decode_kernel2(rmfht::Params<float> pr
     for (long long base = (long long)blockIdx.x * nwarps; base < items; base += stride) {
         const long long item = base + warp;
         if (item < items) {
-            const long long f = item / prm.M;
-            const int a = (int)(item % prm.M);
             cp_async_wait_all();
             __syncwarp();
             prefetch_recs(item + stride, cur ^ 1);
 #pragma unroll
             for (int s = 0; s < C::NS; s++) cx.ach[s] = alpha_w[lane + 32 * s];
-            (void)f;
             const uint16_t* recs = ws.recs[cur];
             for (int s = lane; s < S; s += 32) {
                 const int mn = s < L ? MM : MM - (s - L) / (2 * L);

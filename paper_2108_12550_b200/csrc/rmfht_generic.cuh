@@ -427,7 +427,6 @@ __device__ int walk(W<T>& w, int P0) {
     int sp = 0;
     st[0] = Frame{(int8_t)w.sh.r, (int8_t)MM, 0, 0, (int16_t)P0, 0};
     int ret_P = P0;
-    uint8_t* ret_out = nullptr;
     while (sp >= 0) {
         Frame& fr = st[sp];
         const int s = fr.s, r = fr.r, n = 1 << s;

@@ -259,7 +259,10 @@ class StreamDecoder:
         self.torch, self.plan, self.batch, self.seed, self.ident = torch, plan, batch, seed, identity_root
         dev = torch.device("cuda")
         self.compute = torch.cuda.Stream()
-        self.copy = torch.cuda.Stream()
+        # one stream per direction: an H2D queued behind the previous batch's
+        # D2H (which waits for that decode) would serialise copy and decode
+        self.h2d = torch.cuda.Stream()
+        self.d2h = torch.cuda.Stream()
         self.depth = depth
         self.d_llr = [torch.empty((batch, plan.N), dtype=torch.float32, device=dev) for _ in range(depth)]
         self.out = [plan.alloc_outputs(batch, dev) for _ in range(depth)]
@@ -284,10 +287,10 @@ class StreamDecoder:
             ev.synchronize()
             # buffer j is reused right below: hand out a snapshot
             ready = {k: v[:nj].clone() for k, v in self.h_out[j].items()}
-        with torch.cuda.stream(self.copy):
-            self.copy.wait_event(self.done[i])  # buffer i free (its previous decode finished)
+        with torch.cuda.stream(self.h2d):
+            self.h2d.wait_event(self.done[i])  # buffer i free (its previous decode finished)
             self.d_llr[i][:n].copy_(h_llr, non_blocking=True)
-            self.in_ready[i].record(self.copy)
+            self.in_ready[i].record(self.h2d)
         with torch.cuda.stream(self.compute):
             self.compute.wait_event(self.in_ready[i])
             self.compute.wait_event(self.out_ready[i])  # previous results of buffer i copied out
@@ -295,11 +298,11 @@ class StreamDecoder:
             self.plan.launch_sampled(self.d_llr[i][:n], self.seed, out, frame0=self.frame0,
                                      identity_root=self.ident, stream=self.compute)
             self.done[i].record(self.compute)
-        with torch.cuda.stream(self.copy):
-            self.copy.wait_event(self.done[i])
+        with torch.cuda.stream(self.d2h):
+            self.d2h.wait_event(self.done[i])
             for key in ("cw", "pm", "attempt"):
                 self.h_out[i][key][:n].copy_(self.out[i][key][:n], non_blocking=True)
-            self.out_ready[i].record(self.copy)
+            self.out_ready[i].record(self.d2h)
         self.pending.append((i, self.out_ready[i], n))
         self.k += 1
         self.frame0 += n

@@ -214,13 +214,66 @@ def _allreduce(vals, group):
     return [int(v) for v in t.cpu().tolist()]
 
 
-def run_job(job: SimJob, decode_fn=None, rank: int = 0, world: int = 1, group=None) -> list:
-    """Simulate every SNR point; returns one FerRecord each (harness.py:116-165)."""
+class DeviceSimulator:
+    """The GPU pipeline of one job, with no host frames: per batch,
+    rmfht_gen_frames -> decode (on-device permutation tables) ->
+    rmfht_count_errors into a device counter."""
+
+    def __init__(self, spec, cfg: DecoderConfig, batch: int, device=None):
+        import torch
+        self.torch, self.spec = torch, spec
+        self.dec = GpuDecoder(spec, cfg, device)
+        dev = self.dec.device
+        self.llr = torch.empty((batch, spec.N), dtype=torch.float32, device=dev)
+        self.tx = torch.empty((batch, self.dec.plan.words), dtype=torch.int32, device=dev)
+        self.out = self.dec.plan.alloc_outputs(batch, dev)
+        self.counts = torch.zeros(2, dtype=torch.int64, device=dev)
+
+    def run_batch(self, chan: ChannelConfig, point: int, frame0: int, size: int, table_seed: int,
+                  zero_noise: bool = False) -> None:
+        """Queue one batch (stream-ordered; counts accumulate on the device)."""
+        from .channel_model import count_errors_device, gen_frames_device
+        llr, tx = self.llr[:size], self.tx[:size]
+        out = {k: v[:size] for k, v in self.out.items()}
+        gen_frames_device(self.spec, chan, point, frame0, llr, tx, zero_noise)
+        if self.dec.perms:
+            self.dec.plan.launch_sampled(llr, table_seed, out, frame0=frame0, identity_root=True)
+        else:
+            self.dec.plan.launch(llr, None, out)
+        count_errors_device(self.spec, llr, tx, out["cw"], self.counts)
+
+    def take_counts(self):
+        """[frame errors, ML errors] since the last call (synchronises)."""
+        c = [int(v) for v in self.counts.cpu().tolist()]
+        self.counts.zero_()
+        return c
+
+
+def run_job(job: SimJob, decode_fn=None, rank: int = 0, world: int = 1, group=None,
+            frames: str = "auto") -> list:
+    """Simulate every SNR point; returns one FerRecord each (harness.py:116-165).
+
+    frames="host": batches drawn on the host (batch_frames) and decoded by
+    `decode_fn` (default: the CUDA decoder), errors counted on the host.
+    frames="device": frames generated, decoded and counted on the GPU
+    (DeviceSimulator; decode_fn must be None).  "auto" = device when
+    decode_fn is None.  Batches are dealt round-robin over `world` ranks and
+    the counts all-reduced after every round (early stop on
+    min_frame_errors is then identical on every rank)."""
     spec = build_code(job.r, job.m)
     cfg = job.decoder
     ops, steps, mem = modeled_cost(job.r, job.m, cfg)
     adds, comps = split_ops(job.r, job.m, cfg, ops)
-    if decode_fn is None:
+    if frames == "auto":
+        frames = "device" if decode_fn is None else "host"
+    if frames not in ("host", "device"):
+        raise ConfigurationError(f"frames must be 'host', 'device' or 'auto', not {frames!r}")
+    if frames == "device" and decode_fn is not None:
+        raise ConfigurationError("frames='device' runs the CUDA decoder; decode_fn must be None")
+    sim = None
+    if frames == "device":
+        sim = DeviceSimulator(spec, cfg, job.batch)
+    elif decode_fn is None:
         decode_fn = GpuDecoder(spec, cfg)
     nb_total = -(-job.max_frames // job.batch)
     records = []
@@ -228,13 +281,17 @@ def run_job(job: SimJob, decode_fn=None, rank: int = 0, world: int = 1, group=No
         chan = ChannelConfig.for_rate(ebn0, spec.rate, job.seed)
         tseed = _table_seed(job.seed, q)
         t0 = time.monotonic()
-        frames = errors = ml_errors = 0
+        frames_n = errors = ml_errors = 0
         b = 0
         while b < nb_total:
             my = [bi for bi in range(b, min(b + world, nb_total)) if bi % world == rank]
             loc = [0, 0, 0]
             for bi in my:
                 size = min(job.batch, job.max_frames - bi * job.batch)
+                if sim is not None:
+                    sim.run_batch(chan, q, bi * job.batch, size, tseed, job.zero_noise)
+                    loc[0] += size
+                    continue
                 x, llr = batch_frames(spec, chan, job.seed, q, bi, size, job.zero_noise)
                 xhat = decode_fn(llr, tseed, bi * job.batch)
                 wrong = np.any(xhat != x, axis=1)
@@ -248,9 +305,13 @@ def run_job(job: SimJob, decode_fn=None, rank: int = 0, world: int = 1, group=No
                 loc[0] += size
                 loc[1] += int(wrong.sum())
                 loc[2] += ml
+            if sim is not None:
+                e, ml = sim.take_counts()
+                loc[1] += e
+                loc[2] += ml
             if world > 1:
                 loc = _allreduce(loc, group)
-            frames += loc[0]
+            frames_n += loc[0]
             errors += loc[1]
             ml_errors += loc[2]
             b += world
@@ -259,7 +320,7 @@ def run_job(job: SimJob, decode_fn=None, rank: int = 0, world: int = 1, group=No
         wall = time.monotonic() - t0
         records.append(FerRecord(
             r=job.r, m=job.m, decoder=cfg.algorithm, L=cfg.L, M=cfg.M, P=cfg.P, ebn0_db=float(ebn0),
-            frames=frames, frame_errors=errors, fer=errors / frames, ml_lb_fer=ml_errors / frames,
+            frames=frames_n, frame_errors=errors, fer=errors / frames_n, ml_lb_fer=ml_errors / frames_n,
             avg_additions=float(adds), avg_comparisons=float(comps), time_steps=steps, mem_bits=mem,
             wall_seconds=wall, seed=job.seed))
     return records

@@ -36,6 +36,10 @@ def test_fer_matches_reference_monte_carlo(name):
         lo, hi = harness.clopper_pearson(ref["errors"], ref["frames"], alpha=1e-3)
         glo, ghi = harness.clopper_pearson(rec.frame_errors, rec.frames, alpha=1e-3)
         assert ghi >= lo and glo <= hi
+        # ML lower bound (harness.py:79-84): same test on its counts
+        ml, ref_ml = round(rec.ml_lb_fer * rec.frames), round(ref["ml_lb_fer"] * ref["frames"])
+        p = fisher_exact([[ml, rec.frames - ml], [ref_ml, ref["frames"] - ref_ml]]).pvalue
+        assert p > 1e-3, (name, rec.ebn0_db, ml, rec.frames, ref_ml, ref["frames"])
 
 
 def test_gpu_harness_zero_noise_and_rank_invariance():

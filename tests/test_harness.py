@@ -51,6 +51,15 @@ def test_job_validation():
             _job(**kw)
 
 
+def test_frames_mode_validation():
+    spec = build_code(2, 5)
+    cfg = DecoderConfig("p-FHT-FSCL", L=4, M=2)
+    with pytest.raises(ConfigurationError):
+        harness.run_job(_job(), decode_fn=OracleDecode(spec, cfg), frames="device")
+    with pytest.raises(ConfigurationError):
+        harness.run_job(_job(), decode_fn=OracleDecode(spec, cfg), frames="disk")
+
+
 def test_modeled_costs_match_reference():
     path = os.path.join(GOLDEN, "ref_fer.json")
     if not os.path.exists(path):

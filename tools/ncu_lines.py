@@ -18,24 +18,9 @@ for r in rows[2:]:
         val = int(r[iE] or 0) if metric == "exec" else int(r[iW] or 0)
         execs.append((int(r[iA], 16), r[iS].strip(), val))
 base = execs[0][0]
-d = tempfile.mkdtemp()
-subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=d, capture_output=True)
-cub = glob.glob(os.path.join(d, "*.cubin"))[0]
-dis = subprocess.run(["nvdisasm", "--print-line-info", cub], capture_output=True, text=True).stdout
-line_of = {}
-fn, cur = None, None
-for ln in dis.splitlines():
-    m = re.match(r"\s*\.text\.(\S+):", ln)
-    if m:
-        fn = m.group(1)
-        continue
-    m = re.search(r'//## File "([^"]+)", line (\d+)', ln)
-    if m:
-        cur = (os.path.basename(m.group(1)), int(m.group(2)))
-        continue
-    m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(\S.*)", ln)
-    if m and fn and ksub in fn:
-        line_of[int(m.group(1), 16)] = cur
+sys.path.insert(0, os.path.dirname(__file__))
+from sassmap import line_map, func_of
+line_of = line_map(obj, ksub)
 cnt = collections.Counter()
 miss = 0
 for addr, src, n in execs:
@@ -53,3 +38,10 @@ for (f, l), n in cnt.most_common(top):
         srcs[f] = open(p[0]).read().split("\n") if p else []
     txt = srcs[f][l - 1].strip()[:80] if srcs[f] and l <= len(srcs[f]) else ""
     print(f"{n / items:7.1f}  {f}:{l}  {txt}")
+
+fcnt = collections.Counter()
+for (f, l), n in cnt.items():
+    fcnt[func_of(f, l)] += n
+print("-- by enclosing function")
+for nm, n in fcnt.most_common(top):
+    print(f"{n / items:7.1f}  {nm}")
