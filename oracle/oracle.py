@@ -34,6 +34,9 @@ def lib():
             fn = getattr(_lib, f"rmo_decode_{sfx}")
             fn.restype = ctypes.c_int
             fn.argtypes = [ctypes.c_int] * 6 + [P, ctypes.c_long, P, ctypes.c_int] + [P] * 7
+            fa = getattr(_lib, f"rmo_aut_ssc_{sfx}")
+            fa.restype = ctypes.c_int
+            fa.argtypes = [ctypes.c_int] * 3 + [P, ctypes.c_long, P, ctypes.c_int, P, P, P]
         _lib.rmo_maps_per_attempt.restype = ctypes.c_int
         _lib.rmo_maps_per_attempt.argtypes = [ctypes.c_int] * 4 + [P]
         _lib.rmo_expand_table.restype = ctypes.c_int
@@ -93,3 +96,24 @@ def decode(r, m, L, M, llr, raw_maps=None, perms=True, dtype=np.float64, tie_fix
         raise RuntimeError(f"oracle decode failed rc={rc}")
     return dict(cw=cw, pm=pm, attempt=att, path=path, att_pm=att_pm, att_cw=att_cw,
                 margin=margin)
+
+
+def aut_ssc(r, m, P, llr, raw_maps, dtype=np.float64, nthreads=1):
+    """Aut-SSC (top_decoders.py:235-249) on the CPU oracle: P SSC decodes per
+    frame under the maps raw_maps (B, P, m+1); returns dict(cw, score, winner)."""
+    dtype = np.dtype(dtype)
+    llr = np.ascontiguousarray(llr, dtype=dtype)
+    B, N = llr.shape
+    if N != 1 << m:
+        raise ValueError(f"LLR length {N} != {1 << m}")
+    raw_maps = np.ascontiguousarray(raw_maps, dtype=np.uint16)
+    if raw_maps.shape != (B, P, m + 1):
+        raise ValueError(f"raw_maps shape {raw_maps.shape} != {(B, P, m + 1)}")
+    cw = np.zeros((B, N), dtype=np.uint8)
+    score = np.zeros(B, dtype=dtype)
+    win = np.zeros(B, dtype=np.int32)
+    fn = lib().rmo_aut_ssc_f64 if dtype == np.float64 else lib().rmo_aut_ssc_f32
+    rc = fn(r, m, P, _ptr(llr), B, _ptr(raw_maps), int(nthreads), _ptr(cw), _ptr(score), _ptr(win))
+    if rc != 0:
+        raise RuntimeError(f"oracle aut_ssc failed rc={rc}")
+    return dict(cw=cw, score=score, winner=win)

@@ -593,4 +593,85 @@ int FN(rmo_decode)(int r, int m, int L, int M, int perms, int flags, const REAL 
     return err;
 }
 
+/* ---------------------------------------------------------- Aut-SSC ----
+ * ssc_decode, top_decoders.py:205-230: simplified SC with rate-0 (r < 0),
+ * rate-1 (r == m), repetition (r == 0: all ones iff np.sum(a) < 0, numpy
+ * pairwise order) and SPC (r == m-1: hard decisions, and on odd parity the
+ * first minimum of |a| flipped) leaves; f, g and propagate_hard otherwise.
+ * `out` receives the node's n bits; `scratch` holds >= n reals. */
+static void FN(ssc)(int r, int m, const REAL *a, uint8_t *out, REAL *scratch)
+{
+    const int n = 1 << m;
+    if (r < 0) { memset(out, 0, (size_t)n); return; }
+    if (r == m) { for (int i = 0; i < n; i++) out[i] = a[i] < 0; return; }
+    if (r == 0) { memset(out, FN(pw_sum)(a, n) < 0 ? 1 : 0, (size_t)n); return; }
+    if (r == m - 1) {
+        int par = 0, amin = 0;
+        REAL best = 0;
+        for (int i = 0; i < n; i++) {
+            out[i] = a[i] < 0;
+            par ^= out[i];
+            REAL v = a[i] < 0 ? -a[i] : a[i];
+            if (i == 0 || v < best) { best = v; amin = i; }   /* np.argmin: first minimum */
+        }
+        if (par) out[amin] ^= 1;
+        return;
+    }
+    const int h = n >> 1;
+    REAL *x = scratch;
+    for (int i = 0; i < h; i++) x[i] = FN(f_op)(a[i], a[h + i]);
+    FN(ssc)(r - 1, m - 1, x, out, scratch + h);
+    for (int i = 0; i < h; i++) x[i] = FN(g_op)(a[i], a[h + i], out[i]);
+    FN(ssc)(r, m - 1, x, out + h, scratch + h);
+    for (int i = 0; i < h; i++) out[i] ^= out[h + i];       /* propagate_hard, list_engine.py:30-36 */
+}
+
+/* aut_ssc, top_decoders.py:235-249, over a batch: P SSC decodes of the
+ * permuted frame (apply_perm: x[sigma(i)] = alpha[i]), each un-permuted
+ * (cand[i] = c[sigma(i)]) and scored by correlation (:231, np.sum of
+ * (1-2 cand) alpha in numpy pairwise order); the first strictly largest
+ * score wins.  raw_maps [B, P, m+1]; outputs cw [B, N], score [B], winner [B]. */
+int FN(rmo_aut_ssc)(int r, int m, int P, const REAL *llr, long B, const uint16_t *raw_maps, int nthreads,
+                    uint8_t *cw_out, REAL *score_out, int32_t *winner_out)
+{
+    if (m < 2 || m > RMO_MAXM || r < 1 || r > m - 1 || P < 1) return -3;
+    const int N = 1 << m;
+    int err = 0;
+#ifdef _OPENMP
+#pragma omp parallel num_threads(nthreads > 0 ? nthreads : 1) reduction(min : err)
+#endif
+    {
+        REAL *x = (REAL *)malloc(sizeof(REAL) * (size_t)N * 3);
+        REAL *scr = x + N, *sv = x + 2 * N;
+        uint8_t *c = (uint8_t *)malloc((size_t)N * 2), *cand = c + N;
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 2)
+#endif
+        for (long f = 0; f < B; f++) {
+            const REAL *al = llr + (size_t)f * N;
+            REAL best = 0;
+            int win = -1;
+            for (int p = 0; p < P; p++) {
+                rmo_map mp;
+                if (rmo_expand(raw_maps + ((size_t)f * P + p) * (size_t)(m + 1), m, m, &mp) != 0) { err = -4; continue; }
+                for (int i = 0; i < N; i++) x[rmo_fwd(&mp, (unsigned)i)] = al[i];
+                FN(ssc)(r, m, x, c, scr);
+                for (int i = 0; i < N; i++) cand[i] = c[rmo_fwd(&mp, (unsigned)i)];
+                for (int i = 0; i < N; i++) sv[i] = cand[i] ? -al[i] : al[i];
+                const REAL sc = FN(pw_sum)(sv, N);
+                if (win < 0 || sc > best) {              /* score > best_score, best starts at -inf */
+                    best = sc;
+                    win = p;
+                    memcpy(cw_out + (size_t)f * N, cand, (size_t)N);
+                }
+            }
+            score_out[f] = best;
+            if (winner_out) winner_out[f] = win;
+        }
+        free(c);
+        free(x);
+    }
+    return err;
+}
+
 #undef FN

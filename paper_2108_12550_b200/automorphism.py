@@ -100,6 +100,20 @@ def gf2_invertible_masks(masks: np.ndarray, m: int) -> np.ndarray:
     return ok.reshape(np.shape(masks)[:-1])
 
 
+def sample_affine(m: int, rng: np.random.Generator) -> AffineMap:
+    """Reference-stream replay of ``sample_affine`` (automorphism.py:127-141):
+    m row masks per candidate until invertible, then b — the draws aut_ssc
+    makes once per decode."""
+    if m < 1:
+        raise ValueError("m must be >= 1")
+    while True:
+        masks = rng.integers(0, 1 << m, size=m, dtype=np.int64)
+        if gf2_invertible_masks(masks[None, :], m)[0]:
+            break
+    b = int(rng.integers(0, 1 << m))
+    return AffineMap.from_masks(masks, b, m)
+
+
 def sample_affine_batch(m: int, count: int, rng: np.random.Generator) -> list:
     """Reference-stream replay of ``sample_affine_batch`` (automorphism.py:144-161)."""
     if m < 1:

@@ -30,6 +30,21 @@ def load_golden(name):
     return out
 
 
+def aut_names():
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "autssc_*.npz")))
+
+
+def load_aut(name):
+    """Aut-SSC fixture (tools/gen_golden.py run_aut_case)."""
+    d = np.load(os.path.join(GOLDEN, name + ".npz"))
+    out = {k: d[k] for k in d.files}
+    for k in ("r", "m", "P"):
+        out[k] = int(out[k])
+    out["mode"] = str(out["mode"])
+    out["cw_bits"] = np.unpackbits(out["cw"], axis=-1, bitorder="little")[..., :1 << out["m"]]
+    return out
+
+
 @pytest.fixture(scope="session")
 def oracle_mod():
     from oracle import oracle

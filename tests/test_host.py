@@ -47,13 +47,26 @@ def test_polar_codewords():
 
 def test_sampler_replays_reference_stream():
     d = np.load(os.path.join(GOLDEN, "sampler_stream.npz"))
-    for key in [k for k in d.files if not k.endswith(("_next", "_perm0"))]:
+    for key in [k for k in d.files if not k.endswith(("_next", "_perm0")) and not k.startswith("single_")]:
         m, count, seed = (int(t[1:]) for t in key.split("_"))
         g = np.random.default_rng(seed)
         maps = aut.sample_affine_batch(m, count, g)
         assert np.array_equal(aut.maps_to_raw(maps, m), d[key])
         assert np.array_equal(g.integers(0, 2 ** 31, size=4), d[key + "_next"])  # same draws consumed
         assert np.array_equal(maps[0].perm, d[key + "_perm0"])
+
+
+def test_single_sampler_replays_reference_stream():
+    """sample_affine (automorphism.py:127-141), the per-decode draw of aut_ssc."""
+    d = np.load(os.path.join(GOLDEN, "sampler_stream.npz"))
+    keys = [k for k in d.files if k.startswith("single_") and not k.endswith("_next")]
+    assert keys
+    for key in keys:
+        m, count, seed = (int(t[1:]) for t in key.split("_")[1:])
+        g = np.random.default_rng(seed)
+        maps = [aut.sample_affine(m, g) for _ in range(count)]
+        assert np.array_equal(aut.maps_to_raw(maps, m), d[key])
+        assert np.array_equal(g.integers(0, 2 ** 31, size=4), d[key + "_next"])
 
 
 def test_random_table_is_invertible_and_uniform_shape():

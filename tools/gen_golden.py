@@ -38,8 +38,10 @@ sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 from rmworkbench import rm_core as ref_core  # noqa: E402
 from rmworkbench.automorphism import AffinePermutation, sample_affine_batch  # noqa: E402
 from rmworkbench.channel_model import ChannelConfig, frame_rng, llr, transmit  # noqa: E402
-from rmworkbench.top_decoders import (ensemble_decode, fht_fsc_decode,  # noqa: E402
-                                      fht_fscl_decode, p_fht_fscl)
+from rmworkbench.top_decoders import (aut_ssc, correlation, ensemble_decode,  # noqa: E402
+                                      fht_fsc_decode, fht_fscl_decode, p_fht_fscl,
+                                      ssc_decode)
+from rmworkbench.automorphism import apply_perm, apply_perm_inverse, sample_affine  # noqa: E402
 
 from paper_2108_12550_b200 import automorphism as host_aut  # noqa: E402
 from paper_2108_12550_b200.plan import map_sizes  # noqa: E402
@@ -72,6 +74,48 @@ CASES = {
     "rm38_L4_M4_exact": (3, 8, 4, 4, True, 6, "exact31", 2.0, 4, {}),
     "rm29_L2_M8_channel": (2, 9, 2, 8, True, 8, "channel", 2.5, 2, {}),
 }
+
+
+# Aut-SSC (top_decoders.py:235-249): name: (r, m, P, frames, mode, ebn0)
+AUT_CASES = {
+    "autssc_rm12_P4_exact": (1, 2, 4, 32, "exact31", 2.0),
+    "autssc_rm15_P3_zero": (1, 5, 3, 24, "zero", 3.0),
+    "autssc_rm25_P8_exact": (2, 5, 8, 48, "exact31", 2.0),
+    "autssc_rm27_P16_channel": (2, 7, 16, 256, "channel", 2.0),
+    "autssc_rm28_P64_channel": (2, 8, 64, 64, "channel", 2.0),
+    "autssc_rm38_P32_exact": (3, 8, 32, 48, "exact31", 2.5),
+    "autssc_rm48_P16_channel": (4, 8, 16, 48, "channel", 3.0),
+    "autssc_rm29_P32_channel": (2, 9, 32, 32, "channel", 2.0),
+    "autssc_rm310_P8_channel": (3, 10, 8, 16, "channel", 3.0),
+}
+
+
+def run_aut_case(name, r, m, P, frames, mode, ebn0):
+    """The reference's aut_ssc on a replayed table, plus its per-decode scores
+    (ssc_decode / apply_perm / correlation, the same calls aut_ssc makes)."""
+    spec = ref_core.build_code(r, m)
+    llrs, xs = make_llrs(spec, frames, mode, ebn0)
+    rng = np.random.default_rng(zlib.crc32(name.encode()))
+    raw = host_aut.random_raw_table(rng, (frames, P), [m], m).reshape(frames, P, m + 1)
+    cw = np.zeros((frames, spec.N), dtype=np.uint8)
+    score = np.zeros(frames)
+    winner = np.zeros(frames, dtype=np.int32)
+    scores = np.zeros((frames, P))
+    for f in range(frames):
+        alpha = llrs[f].astype(np.float64)
+        maps = [to_ref_perm(p) for p in host_aut.raw_to_maps(raw[f], [m] * P)]
+        res = aut_ssc(spec, alpha, P, None, sampler=replay_sampler(maps))
+        best, bs = -1, -np.inf
+        for p, perm in enumerate(maps):
+            cand = apply_perm_inverse(perm, ssc_decode(spec, apply_perm(perm, alpha)).codeword)
+            scores[f, p] = correlation(cand, alpha)
+            if scores[f, p] > bs:
+                best, bs = p, scores[f, p]
+        assert np.array_equal(res.codeword, apply_perm_inverse(
+            maps[best], ssc_decode(spec, apply_perm(maps[best], alpha)).codeword)), name
+        cw[f], score[f], winner[f] = res.codeword, bs, best
+    return dict(r=r, m=m, P=P, mode=mode, ebn0=ebn0, llr=llrs, x=xs, raw=raw, scores=scores,
+                cw=np.packbits(cw, axis=-1, bitorder="little"), score=score, winner=winner)
 
 
 def make_llrs(spec, frames, mode, ebn0, seed=777, q=0):
@@ -160,6 +204,12 @@ def sampler_stream_fixture():
         out[f"m{m}_c{count}_s{seed}"] = raw
         out[f"m{m}_c{count}_s{seed}_next"] = g.integers(0, 2 ** 31, size=4)
         out[f"m{m}_c{count}_s{seed}_perm0"] = maps[0].perm
+    # single draws (sample_affine, automorphism.py:127-141), as aut_ssc makes them
+    for m, count, seed in [(9, 6, 7), (5, 10, 8), (2, 12, 9), (8, 5, 10)]:
+        g = np.random.default_rng(seed)
+        maps = [sample_affine(m, g) for _ in range(count)]
+        out[f"single_m{m}_c{count}_s{seed}"] = host_aut.maps_to_raw(maps, m)
+        out[f"single_m{m}_c{count}_s{seed}_next"] = g.integers(0, 2 ** 31, size=4)
     return out
 
 
@@ -174,6 +224,12 @@ def main():
         t0 = time.time()
         d = run_case(name, r, m, L, M, perms, frames, mode, ebn0, ident)
         np.savez_compressed(os.path.join(OUT, name + ".npz"), **d)
+        print(f"{name}: {frames} frames in {time.time() - t0:.1f}s", flush=True)
+    for name, (r, m, P, frames, mode, ebn0) in AUT_CASES.items():
+        if args.only and args.only not in (name, "aut"):
+            continue
+        t0 = time.time()
+        np.savez_compressed(os.path.join(OUT, name + ".npz"), **run_aut_case(name, r, m, P, frames, mode, ebn0))
         print(f"{name}: {frames} frames in {time.time() - t0:.1f}s", flush=True)
     if not args.only or args.only == "sampler":
         np.savez_compressed(os.path.join(OUT, "sampler_stream.npz"), **sampler_stream_fixture())
