@@ -44,24 +44,32 @@ CONFIGS = {
     "rm37_L8_M32": (3, 7, 8, 32, True, 4.0, 16384),
     "rm29_L1_M512": (2, 9, 1, 512, True, 3.0, 1024),
     "rm25_fhtfsc": (2, 5, 1, 1, False, 3.0, 1048576),
+    # the paper's Table IV comparator, Aut-SSC with P = 512 (M = P here)
+    "rm29_autssc_P512": (2, 9, 1, 512, "aut", 2.5, 2048),
 }
 R, M_VARS, L, M = 2, 9, 4, 20
 PERMS = True
+AUT = False
 EBN0 = 2.5
 WORKLOAD = "RM(2,9) p-FHT-FSCL L=4 M=20 (decoder 0 = identity), Eb/N0 2.5 dB"
 METRIC = "decoded frames/s, RM(2,9) M=20 L=4, 1 B200; % of roofline; vs host CPU"
 
 
 def select_config(name):
-    global R, M_VARS, L, M, PERMS, EBN0, WORKLOAD
+    global R, M_VARS, L, M, PERMS, AUT, EBN0, WORKLOAD
     r, m, l, mm, perms, ebn0, frames = CONFIGS[name]
-    R, M_VARS, L, M, PERMS, EBN0 = r, m, l, mm, perms, ebn0
-    algo = "p-FHT-FSCL" if perms else ("FHT-FSC" if l == 1 else "FHT-FSCL")
-    WORKLOAD = (f"RM({r},{m}) {algo} L={l} M={mm}" + (" (decoder 0 = identity)" if perms else "") +
-                f", Eb/N0 {ebn0} dB")
+    AUT = perms == "aut"
+    R, M_VARS, L, M, PERMS, EBN0 = r, m, l, mm, bool(perms), ebn0
+    algo = "Aut-SSC" if AUT else "p-FHT-FSCL" if perms else ("FHT-FSC" if l == 1 else "FHT-FSCL")
+    if AUT:
+        WORKLOAD = f"RM({r},{m}) Aut-SSC P={mm}, Eb/N0 {ebn0} dB"
+    else:
+        WORKLOAD = (f"RM({r},{m}) {algo} L={l} M={mm}" + (" (decoder 0 = identity)" if perms else "") +
+                    f", Eb/N0 {ebn0} dB")
     global METRIC
     if name != "rm29_L4_M20":
-        METRIC = f"decoded frames/s, RM({r},{m}) {algo} L={l} M={mm}, 1 B200"
+        METRIC = (f"decoded frames/s, RM({r},{m}) Aut-SSC P={mm}, 1 B200" if AUT else
+                  f"decoded frames/s, RM({r},{m}) {algo} L={l} M={mm}, 1 B200")
     return frames
 
 
@@ -131,7 +139,7 @@ def make_inputs(plan, spec, B, seed):
     x, llr = synthetic_frames(spec, EBN0, B, seed)
     recs = None
     if plan.permutations:
-        _, recs = plan.sample(B, seed, identity_root=True, want_raw=False)
+        _, recs = plan.sample(B, seed, identity_root=not AUT, want_raw=False)
     return x, llr, recs
 
 
@@ -145,14 +153,18 @@ def _cpu_batches(B, count, seed0):
     out = []
     for s in range(count):
         _, llr = synthetic_frames(spec, EBN0, B, seed0 + s)
-        raw = (random_raw_table(np.random.default_rng(seed0 + s), (B, M), map_sizes(R, M_VARS, L), M_VARS,
-                                identity_root=L) if PERMS else None)
+        sizes = [M_VARS] if AUT else map_sizes(R, M_VARS, L)
+        raw = (random_raw_table(np.random.default_rng(seed0 + s), (B, M), sizes, M_VARS,
+                                identity_root=0 if AUT else L) if PERMS else None)
         out.append((llr, raw))
     return out
 
 
 def _cpu_decode(llr, raw, cores):
     from oracle import oracle
+    if AUT:
+        oracle.aut_ssc(R, M_VARS, M, llr, raw[:, :, 0, :], dtype=np.float64, nthreads=cores)
+        return
     oracle.decode(R, M_VARS, L, M if PERMS else 1, llr, raw, perms=PERMS, dtype=np.float64, nthreads=cores,
                   want_attempts=False)
 
@@ -223,7 +235,7 @@ def run_gpu(args):
     from paper_2108_12550_b200.rm_core import build_code
 
     spec = build_code(R, M_VARS)
-    plan = Plan(R, M_VARS, L, M, PERMS, "f32", lockstep=0 if args.no_lockstep else args.lockstep)
+    plan = Plan(R, M_VARS, L, M, PERMS, "f32", lockstep=0 if args.no_lockstep else args.lockstep, aut_ssc=AUT)
     B = args.frames
     x, llr, recs = make_inputs(plan, spec, B, seed=1 + rank)  # host table: decode-only timing
     dev = torch.device("cuda", local)
@@ -242,7 +254,7 @@ def run_gpu(args):
     def step():
         # one pass of the hot path: draw the batch's permutations on the device
         # (the reference samples them inside decode) and decode
-        plan.launch_sampled(d_llr, SEED, out, frame0=0, stream=stream)
+        plan.launch_sampled(d_llr, SEED, out, frame0=0, identity_root=not AUT, stream=stream)
 
     for _ in range(args.warmup):
         step()
@@ -284,7 +296,7 @@ def run_gpu(args):
     # the device; H2D of batch k+1 and D2H of batch k-1 overlap decode of k
     from paper_2108_12550_b200.decoder import StreamDecoder
     h_llr = torch.from_numpy(llr).pin_memory()
-    sd = StreamDecoder(plan, B, seed=SEED)
+    sd = StreamDecoder(plan, B, seed=SEED, identity_root=not AUT)
     e_steps = max(3, args.steps)
     for _ in range(2):
         sd.submit(h_llr)
@@ -308,7 +320,11 @@ def run_gpu(args):
     if rank == 0:
         hbm, sm_mhz, src = _peaks()
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        ops = complexity_ops(R, M_VARS, L, M, PERMS, include_perm=True, fsc=not PERMS and L == 1)
+        if AUT:  # accounting.complexity_model("Aut-SSC"): P (SSC ops + N) + P - 1
+            from paper_2108_12550_b200.plan import ssc_ops
+            ops = M * (ssc_ops(R, M_VARS) + spec.N) + M - 1
+        else:
+            ops = complexity_ops(R, M_VARS, L, M, PERMS, include_perm=True, fsc=not PERMS and L == 1)
         peak_gops = sms * 128 * sm_mhz * 1e6 / 1e9
         per_gpu = value / ws
         ach_gops = ops * per_gpu / 1e9

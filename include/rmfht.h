@@ -47,7 +47,12 @@ enum {
     RMFHT_NO_LOCKSTEP = 16,    /* throughput kernel: no barrier between rounds of work items */
     RMFHT_LOCKSTEP_4 = 32,     /* ... barrier per group of 4 warps instead of the whole CTA */
     RMFHT_LOCKSTEP_8 = 64,     /* ... per group of 8 warps */
-    RMFHT_GENERIC = 128        /* use the generic runtime-shaped kernel even if a specialisation exists */
+    RMFHT_GENERIC = 128,       /* use the generic runtime-shaped kernel even if a specialisation exists */
+    RMFHT_AUT_SSC = 256        /* Aut-SSC (aut_ssc, top_decoders.py:235-249): with RMFHT_PERMUTATIONS
+                                  and L = 1, M = P SSC decodes per frame, one map of m variables each
+                                  (S = 1); d_pm receives the winning correlation, d_attempt the
+                                  winning decode (first strictly largest score), d_path 0; the diag
+                                  outputs hold every decode's score and codeword.  m <= 10. */
 };
 
 enum {
@@ -140,7 +145,8 @@ int rmfht_plan_launches_per_call(const rmfht_plan *plan);
 
 /* Which kernel the plan runs: 1 = reference-order (rmfht_kernels.cuh),
  * 2 = float32 throughput kernel (rmfht_fast.cuh), 3 = generic runtime-shaped
- * kernel (rmfht_generic.cuh, reference order); 0 for a NULL plan. */
+ * kernel (rmfht_generic.cuh, reference order), 4 = Aut-SSC (rmfht_ssc.cu);
+ * 0 for a NULL plan. */
 int rmfht_plan_kernel(const rmfht_plan *plan);
 
 const char *rmfht_last_error(void);

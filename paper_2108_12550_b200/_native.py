@@ -18,7 +18,7 @@ INCLUDE = os.path.join(os.path.dirname(_HERE), "include")
 
 RMFHT_F32, RMFHT_F64 = 0, 1
 RMFHT_PERMUTATIONS, RMFHT_TIE_FIX, RMFHT_NO_TIE_FIX, RMFHT_REFERENCE_ORDER, RMFHT_NO_LOCKSTEP = 1, 2, 4, 8, 16
-RMFHT_LOCKSTEP_4, RMFHT_LOCKSTEP_8, RMFHT_GENERIC = 32, 64, 128
+RMFHT_LOCKSTEP_4, RMFHT_LOCKSTEP_8, RMFHT_GENERIC, RMFHT_AUT_SSC = 32, 64, 128, 256
 RMFHT_OK, RMFHT_ECONFIG, RMFHT_EVALUE, RMFHT_EUNSUPPORTED, RMFHT_ECUDA = 0, -1, -2, -3, -4
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
@@ -45,7 +45,8 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
     os.makedirs(objdir, exist_ok=True)
     units = [("rmfht_capi", os.path.join(CSRC, "rmfht_capi.cu"), []),
              ("rmfht_gen", os.path.join(CSRC, "rmfht_gen.cu"), []),
-             ("rmfht_chan", os.path.join(CSRC, "rmfht_chan.cu"), [])]
+             ("rmfht_chan", os.path.join(CSRC, "rmfht_chan.cu"), []),
+             ("rmfht_ssc", os.path.join(CSRC, "rmfht_ssc.cu"), [])]
     for t in ("float", "double"):
         for c in range(4):
             units.append((f"rmfht_bind_{t}_{c}", os.path.join(CSRC, "rmfht_bind.cu"),

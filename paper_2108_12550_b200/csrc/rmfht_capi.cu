@@ -144,6 +144,41 @@ int rmfht_plan_create(int r, int m, int L, int M, int flags, int dtype, rmfht_pl
     if (flags & RMFHT_LOCKSTEP_8) p->lockstep = 8;
     if (flags & RMFHT_TIE_FIX) p->tie_fix = 1;
     if (flags & RMFHT_NO_TIE_FIX) p->tie_fix = 0;
+    if (flags & RMFHT_AUT_SSC) {
+        // Aut-SSC (top_decoders.py:235-249): P = M SSC decodes, one map of m variables each
+        if (L != 1 || !(flags & RMFHT_PERMUTATIONS)) {
+            delete p;
+            return fail(RMFHT_ECONFIG, "Aut-SSC plans take L = 1 and RMFHT_PERMUTATIONS (P = M decodes)");
+        }
+        p->aut = 1;
+        p->fast = 0;
+        p->sizes.assign(1, m);
+        p->S = 1;
+        const int rc = rmfht_bind_aut_ssc(p);
+        if (rc != 0) {
+            delete p;
+            return fail(RMFHT_EUNSUPPORTED, "Aut-SSC supports m <= 10");
+        }
+        *out = p;
+        return 0;
+    }
+    if (flags & RMFHT_AUT_SSC) {
+        // Aut-SSC (top_decoders.py:235-249): P = M SSC decodes, one map of m variables each
+        if (L != 1 || !(flags & RMFHT_PERMUTATIONS)) {
+            delete p;
+            return fail(RMFHT_ECONFIG, "Aut-SSC plans take L = 1 and RMFHT_PERMUTATIONS (P = M decodes)");
+        }
+        p->aut = 1;
+        p->fast = 0;
+        p->sizes.assign(1, m);
+        p->S = 1;
+        if (rmfht_bind_aut_ssc(p) != 0) {
+            delete p;
+            return fail(RMFHT_EUNSUPPORTED, "Aut-SSC supports m <= 10");
+        }
+        *out = p;
+        return 0;
+    }
     if (p->perms) {
         for (int l = 0; l < L; l++) p->sizes.push_back(m);
         if (m - r >= 2)
@@ -174,7 +209,7 @@ int rmfht_plan_record_u16(const rmfht_plan* p) { return p ? 2 * p->m + 2 : fail(
 
 int rmfht_plan_launches_per_call(const rmfht_plan* p) { return p ? (p->fast ? 2 : 1) : 0; }  // + 1 when sampled
 
-int rmfht_plan_kernel(const rmfht_plan* p) { return p ? (p->fast ? 2 : (p->generic ? 3 : 1)) : 0; }
+int rmfht_plan_kernel(const rmfht_plan* p) { return p ? (p->aut ? 4 : p->fast ? 2 : (p->generic ? 3 : 1)) : 0; }
 
 int rmfht_expand_maps(const rmfht_plan* p, const uint16_t* raw, uint16_t* rec, long long count) {
     if (!p) return fail(RMFHT_EVALUE, "plan is NULL");

@@ -20,6 +20,7 @@ struct rmfht_plan {
     int fast;  // float32 throughput kernel (rmfht_fast.cuh) instead of the reference-order one
     int generic = 0;  // runtime-shaped interpreter kernel (rmfht_generic.cuh)
     int force_generic = 0;
+    int aut = 0;  // Aut-SSC plan (RMFHT_AUT_SSC): M = P single-map SSC decodes per frame
     int S, nwarps, grid;
     size_t smem;
     std::vector<int> sizes;
@@ -62,3 +63,4 @@ int fail(int code, const std::string& msg);
 RMFHT_DECL_BINDERS(float)
 RMFHT_DECL_BINDERS(double)
 int rmfht_bind_generic(rmfht_plan* p);
+int rmfht_bind_aut_ssc(rmfht_plan* p);

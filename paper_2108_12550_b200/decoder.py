@@ -43,7 +43,7 @@ class Plan:
 
     def __init__(self, r: int, m: int, L: int, M: int = 1, permutations: bool = True,
                  dtype: str = "f32", tie_fix: bool | None = None, reference_order: bool = False,
-                 lockstep: int = 16, generic: bool = False):
+                 lockstep: int = 16, generic: bool = False, aut_ssc: bool = False):
         build_code(r, m)
         if L < 1 or M < 1:
             raise ConfigurationError("L, M and P must all be >= 1")
@@ -67,6 +67,12 @@ class Plan:
             flags |= _native.RMFHT_LOCKSTEP_8
         if generic:
             flags |= _native.RMFHT_GENERIC
+        if aut_ssc:
+            # Aut-SSC: M = P single-map SSC decodes per frame (RMFHT_AUT_SSC)
+            if L != 1 or not self.permutations:
+                raise ConfigurationError("Aut-SSC plans take L = 1 with permutations (P = M decodes)")
+            flags |= _native.RMFHT_AUT_SSC
+        self.aut_ssc = bool(aut_ssc)
         lib = _native.lib()
         h = ctypes.c_void_p()
         _check(lib.rmfht_plan_create(r, m, L, M, flags,
@@ -81,7 +87,7 @@ class Plan:
         self.rec_u16 = lib.rmfht_plan_record_u16(h)
         self.words = max(1, self.N // 32)
         self.launches_per_call = lib.rmfht_plan_launches_per_call(h)
-        self.kernel = lib.rmfht_plan_kernel(h)  # 1 reference-order, 2 float32 throughput
+        self.kernel = lib.rmfht_plan_kernel(h)  # 1 reference-order, 2 float32 throughput, 3 generic, 4 Aut-SSC
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -214,8 +220,9 @@ def unpack_bits(words: np.ndarray, n: int) -> np.ndarray:
 
 
 @lru_cache(maxsize=64)
-def get_plan(r: int, m: int, L: int, M: int, permutations: bool = True, dtype: str = "f32") -> Plan:
-    return Plan(r, m, L, M, permutations, dtype)
+def get_plan(r: int, m: int, L: int, M: int, permutations: bool = True, dtype: str = "f32",
+             aut_ssc: bool = False) -> Plan:
+    return Plan(r, m, L, M, permutations, dtype, aut_ssc=aut_ssc)
 
 
 @dataclass

@@ -30,7 +30,7 @@ from math import ceil, log2
 import numpy as np
 
 from .channel_model import ChannelConfig
-from .plan import complexity_ops, plan_visits
+from .plan import complexity_ops, plan_visits, ssc_ops, ssc_steps
 from .rm_core import ConfigurationError, build_code, polar_transform
 from .top_decoders import SUPPORTED, DecoderConfig
 
@@ -99,6 +99,11 @@ def modeled_cost(r: int, m: int, cfg: DecoderConfig):
     """(ops, time_steps, mem_bits): complexity_model, latency_total,
     memory_model (accounting.py:189-227, 323-347)."""
     algo = cfg.algorithm
+    if algo == "Aut-SSC":
+        # accounting.py:195-197, 214-216, 338-339
+        N, P = 1 << m, cfg.P
+        steps = ssc_steps(r, m) + (int(ceil(log2(P))) if P > 1 else 0)
+        return P * (ssc_ops(r, m) + N) + (P - 1), steps, (P + 1) * N * 32 + P * N
     perms = algo == "p-FHT-FSCL"
     ops = complexity_ops(r, m, cfg.L if algo != "FHT-FSC" else 1, cfg.M if perms else 1, perms,
                          include_perm=False, fsc=algo == "FHT-FSC")
@@ -138,7 +143,9 @@ def modeled_cost(r: int, m: int, cfg: DecoderConfig):
 
 
 def split_ops(r: int, m: int, cfg: DecoderConfig, total: int):
-    """harness._split_ops (harness.py:233-256): additions vs comparisons."""
+    """harness._split_ops (harness.py:172-195): additions vs comparisons."""
+    if cfg.algorithm == "Aut-SSC":
+        return total, 0  # no _ALGO_FLAGS entry: everything counts as additions
     perms = cfg.algorithm == "p-FHT-FSCL"  # the model follows the algorithm's flags (accounting._ALGO_FLAGS)
     eff_l = 1 if cfg.algorithm == "FHT-FSC" else cfg.L
     comps = 0
@@ -185,10 +192,15 @@ class GpuDecoder:
         import torch
         from .decoder import Plan
         self.torch = torch
-        perms = cfg.algorithm == "p-FHT-FSCL" and cfg.permutations_enabled
-        L = 1 if cfg.algorithm == "FHT-FSC" else cfg.L
-        self.plan = Plan(spec.r, spec.m, L, cfg.M if perms else 1, perms, "f32")
-        self.perms = perms
+        if cfg.algorithm == "Aut-SSC":
+            # P permutations drawn on the device, none of them the identity
+            self.plan = Plan(spec.r, spec.m, 1, cfg.P, True, "f32", aut_ssc=True)
+            self.perms, self.ident = True, False
+        else:
+            perms = cfg.algorithm == "p-FHT-FSCL" and cfg.permutations_enabled
+            L = 1 if cfg.algorithm == "FHT-FSC" else cfg.L
+            self.plan = Plan(spec.r, spec.m, L, cfg.M if perms else 1, perms, "f32")
+            self.perms, self.ident = perms, True
         self.device = device or torch.device("cuda", torch.cuda.current_device())
 
     def __call__(self, llr: np.ndarray, table_seed: int, frame0: int):
@@ -196,7 +208,7 @@ class GpuDecoder:
         d_llr = torch.from_numpy(llr).to(self.device)
         out = self.plan.alloc_outputs(llr.shape[0], self.device)
         if self.perms:
-            self.plan.launch_sampled(d_llr, table_seed, out, frame0=frame0, identity_root=True)
+            self.plan.launch_sampled(d_llr, table_seed, out, frame0=frame0, identity_root=self.ident)
         else:
             self.plan.launch(d_llr, None, out)
         words = out["cw"].cpu().numpy().view(np.uint32)
@@ -237,7 +249,7 @@ class DeviceSimulator:
         out = {k: v[:size] for k, v in self.out.items()}
         gen_frames_device(self.spec, chan, point, frame0, llr, tx, zero_noise)
         if self.dec.perms:
-            self.dec.plan.launch_sampled(llr, table_seed, out, frame0=frame0, identity_root=True)
+            self.dec.plan.launch_sampled(llr, table_seed, out, frame0=frame0, identity_root=self.dec.ident)
         else:
             self.dec.plan.launch(llr, None, out)
         count_errors_device(self.spec, llr, tx, out["cw"], self.counts)

@@ -97,3 +97,40 @@ def complexity_ops(r: int, m: int, L: int, M: int, permutations: bool = True,
         elif kind == "perm" and include_perm:
             total += _perm_charge(mm, eff_l)
     return (M if permutations else 1) * total
+
+
+def ssc_walk(r: int, m: int) -> list:
+    """Node visits of ssc_decode (accounting._ssc_walk, accounting.py:232-252):
+    rate0 / rate1 / rep / spc1 leaves, f and g at internal nodes."""
+    visits = []
+
+    def rec(rr: int, mm: int):
+        if rr < 0 or rr == mm or rr == 0 or (mm >= 1 and rr == mm - 1):
+            visits.append(("rate0" if rr < 0 else "rate1" if rr == mm else "rep" if rr == 0 else "spc1", mm))
+            return
+        visits.append(("f", mm))
+        rec(rr - 1, mm - 1)
+        visits.append(("g", mm))
+        rec(rr, mm - 1)
+
+    rec(r, m)
+    return visits
+
+
+def ssc_ops(r: int, m: int) -> int:
+    """accounting._ssc_operations (accounting.py:255-265)."""
+    ops = 0
+    for kind, mm in ssc_walk(r, m):
+        n = 1 << mm
+        if kind in ("f", "g"):
+            ops += n >> 1
+        elif kind == "rep":
+            ops += n - 1
+        elif kind == "spc1":
+            ops += n
+    return ops
+
+
+def ssc_steps(r: int, m: int) -> int:
+    """accounting._ssc_steps (accounting.py:268-273)."""
+    return sum(1 for kind, _ in ssc_walk(r, m) if kind in ("f", "g", "rep", "spc1"))

@@ -2,7 +2,7 @@
 
 Same names, arguments, error types and random-number consumption as
 ``/root/reference/pkg/src/rmworkbench/top_decoders.py`` for the
-p-FHT-FSCL path; decoding itself runs in the CUDA library.  Permutations
+p-FHT-FSCL family and Aut-SSC; decoding itself runs in the CUDA library.  Permutations
 are drawn on the host exactly as the reference draws them (or taken from a
 ``sampler`` plugin, called in the reference's order) and handed to the GPU
 as a table.
@@ -14,14 +14,14 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .automorphism import maps_to_raw, sample_affine_batch
+from .automorphism import maps_to_raw, sample_affine, sample_affine_batch
 from .decoder import get_plan
 from .plan import map_sizes, plan_visits
 from .rm_core import CodeSpec, ConfigurationError
 
 ALGORITHMS = ("SC", "SCL", "FSCL", "FHT-FSC", "FHT-FSCL", "p-FHT-FSCL",
               "Aut-SSC", "RPA", "SRPA")
-SUPPORTED = ("FHT-FSC", "FHT-FSCL", "p-FHT-FSCL")
+SUPPORTED = ("FHT-FSC", "FHT-FSCL", "p-FHT-FSCL", "Aut-SSC")
 
 
 @dataclass(frozen=True)
@@ -152,8 +152,27 @@ def fht_fsc_decode(spec: CodeSpec, alpha, trace=None) -> DecodeResult:
     return fht_fscl_decode(spec, alpha, 1, trace=trace)
 
 
+def aut_ssc(spec: CodeSpec, alpha, P: int, rng, sampler=None) -> DecodeResult:
+    """P SSC decodes under random permutations; the candidate with the
+    largest correlation wins, the first on ties (top_decoders.py:235-249).
+    Maps are drawn one per decode like the reference (sample_affine, or the
+    ``sampler`` plugin).  ``pm`` is NaN as in the reference; ``attempt`` is
+    the winning decode."""
+    if P < 1:
+        raise ConfigurationError("P must be >= 1")
+    alpha = _alpha(spec, alpha)
+    if rng is None and sampler is None:
+        raise ConfigurationError("Aut-SSC needs an rng")
+    maps = [sampler() if sampler is not None else sample_affine(spec.m, rng) for _ in range(P)]
+    plan = get_plan(spec.r, spec.m, 1, P, True, DEFAULT_DTYPE, aut_ssc=True)
+    res = plan.decode(alpha[None, :], raw_maps=maps_to_raw(maps, spec.m).reshape(1, P, 1, spec.m + 1))
+    return DecodeResult(codeword=res["cw"][0].astype(np.uint8), pm=float("nan"),
+                        attempt=int(res["attempt"][0]), path=0)
+
+
 def decode(spec: CodeSpec, alpha, cfg: DecoderConfig, rng) -> DecodeResult:
-    """Dispatch one frame (top_decoders.py:252-271) for the p-FHT-FSCL family."""
+    """Dispatch one frame (top_decoders.py:252-271) for the p-FHT-FSCL family
+    and Aut-SSC."""
     algo = cfg.algorithm
     if algo == "FHT-FSC":
         return fht_fsc_decode(spec, alpha)
@@ -165,5 +184,7 @@ def decode(spec: CodeSpec, alpha, cfg: DecoderConfig, rng) -> DecodeResult:
         if cfg.M > 1:
             return ensemble_decode(spec, alpha, cfg.L, cfg.M, rng)
         return p_fht_fscl(spec, alpha, cfg.L, rng)
+    if algo == "Aut-SSC":
+        return aut_ssc(spec, alpha, cfg.P, rng)
     raise ConfigurationError(f"algorithm {algo!r} is not part of this decoder "
                              f"(supported: {', '.join(SUPPORTED)})")

@@ -24,7 +24,7 @@ def test_fer_matches_reference_monte_carlo(name):
     from paper_2108_12550_b200 import harness
     from paper_2108_12550_b200.top_decoders import DecoderConfig
     job = REF["jobs"][name]
-    cfg = DecoderConfig(job["algorithm"], L=job["L"], M=job["M"])
+    cfg = DecoderConfig(job["algorithm"], L=job["L"], M=job["M"], P=job.get("P", 1))
     pts = tuple(p["ebn0"] for p in job["points"])
     frames = max(200000, 4 * max(p["frames"] for p in job["points"]))
     recs = harness.run_job(harness.SimJob(r=job["r"], m=job["m"], decoder=cfg, ebn0_points=pts, max_frames=frames,

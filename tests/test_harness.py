@@ -66,7 +66,7 @@ def test_modeled_costs_match_reference():
         pytest.skip("reference FER fixture not generated")
     ref = json.load(open(path))
     for name, job in ref["jobs"].items():
-        cfg = DecoderConfig(job["algorithm"], L=job["L"], M=job["M"])
+        cfg = DecoderConfig(job["algorithm"], L=job["L"], M=job["M"], P=job.get("P", 1))
         ops, steps, mem = harness.modeled_cost(job["r"], job["m"], cfg)
         c = ref["costs"][name]
         assert (ops, steps, mem) == (c["ops"], c["steps"], c["mem"]), name

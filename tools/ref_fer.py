@@ -13,6 +13,8 @@ JOBS = [
     ("rm26_fhtfscl_L4", 2, 6, DecoderConfig("FHT-FSCL", L=4), (2.0, 2.5), 40000),
     ("rm26_pfhtfscl_L4", 2, 6, DecoderConfig("p-FHT-FSCL", L=4), (2.0, 2.5), 40000),
     ("rm29_L4_M20", 2, 9, DecoderConfig("p-FHT-FSCL", L=4, M=20), (1.0, 1.5), 6000),
+    ("rm27_autssc_P16", 2, 7, DecoderConfig("Aut-SSC", P=16), (2.0, 3.0), 16000),
+    ("rm28_autssc_P64", 2, 8, DecoderConfig("Aut-SSC", P=64), (2.0, 2.5), 4000),
 ]
 OUT = os.path.join(os.path.dirname(__file__), "..", "tests", "golden", "ref_fer.json")
 only = sys.argv[1] if len(sys.argv) > 1 else None
@@ -24,7 +26,7 @@ for name, r, m, cfg, pts, frames in JOBS:
                  seed=777, workers=os.cpu_count())
     t = time.time()
     recs = run_job(job)
-    out["jobs"][name] = dict(r=r, m=m, algorithm=cfg.algorithm, L=cfg.L, M=cfg.M,
+    out["jobs"][name] = dict(r=r, m=m, algorithm=cfg.algorithm, L=cfg.L, M=cfg.M, P=cfg.P,
                              points=[dict(ebn0=rc.ebn0_db, frames=rc.frames, errors=rc.frame_errors,
                                           ml_lb_fer=rc.ml_lb_fer, wall=rc.wall_seconds) for rc in recs])
     ops, steps, mem = _modeled_cost(job)
