@@ -155,3 +155,14 @@ int BINDER(RMFHT_T, RMFHT_CHUNK)(rmfht_plan* p) {
 #undef X
     return RMFHT_EUNSUPPORTED;
 }
+
+#ifdef RMFHT_STATS
+// diagnostic build only (tools/stats_run.py): read and clear this unit's counters
+#define STATS_(t, n) rmfht_stats_read_##t##_##n
+#define STATS(t, n) STATS_(t, n)
+extern "C" int STATS(RMFHT_T, RMFHT_CHUNK)(unsigned long long* host) {
+    if (cudaMemcpyFromSymbol(host, rmfht2::g_stats, sizeof(rmfht2::g_stats)) != cudaSuccess) return -1;
+    static const unsigned long long zero[256] = {};
+    return cudaMemcpyToSymbol(rmfht2::g_stats, zero, sizeof(zero)) == cudaSuccess ? 0 : -1;
+}
+#endif

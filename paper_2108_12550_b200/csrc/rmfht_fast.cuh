@@ -151,6 +151,15 @@ __device__ __forceinline__ u32 lin_apply(const u32* cols, u32 x) {
     return v;
 }
 
+// order-preserving float <-> uint32 keys (any sign; no NaN)
+__device__ __forceinline__ u32 float_key(float f) {
+    const u32 b = __float_as_uint(f);
+    return b ^ ((b >> 31) ? 0xffffffffu : 0x80000000u);
+}
+__device__ __forceinline__ float key_float(u32 k) {
+    return __uint_as_float(k ^ ((k >> 31) ? 0x80000000u : 0xffffffffu));
+}
+
 // group-local xor reduce / broadcast helpers
 template <int LPP, int ACT>
 __device__ __forceinline__ float group_sum_tree(float v) {
@@ -217,6 +226,16 @@ __device__ __forceinline__ float lds_addr(u32 saddr) {
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(saddr));
     return v;
 }
+
+#ifdef RMFHT_STATS
+// diagnostic counters (tools/stats_run.py builds a separate library with them)
+__device__ unsigned long long g_stats[256];
+#define RMFHT_STAT(i) do { if (lane_id() == 0) atomicAdd(&g_stats[(i)], 1ull); } while (0)
+#define RMFHT_STAT_ADD(i, v) do { if (lane_id() == 0) atomicAdd(&g_stats[(i)], (unsigned long long)(v)); } while (0)
+#else
+#define RMFHT_STAT(i) do { } while (0)
+#define RMFHT_STAT_ADD(i, v) do { } while (0)
+#endif
 
 // Rare path of fht_node (more candidates than kCap): exact K-round selection
 // per path, then the pool — as the reference-order kernel does it.
@@ -352,15 +371,17 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
         }
     }
     // path maximum and the pool threshold tau = L-th smallest path-best pm
+    // (a warp-wide maximum: one REDUX on order-preserving integer keys; cbest
+    // can be a rounding error below zero, llrabs and M1 being summed in
+    // different orders)
     float mx = act ? fabsf(w[0]) : -1.f;
 #pragma unroll
     for (int k = 1; k < V; k++) mx = fmaxf(mx, fabsf(w[k]));
+    constexpr u32 GBITS = (LV::act >= 32) ? 0xffffffffu : ((1u << LV::act) - 1u);  // active lanes of a group
     const float M1 = group_max<LV::act>(mx);
     const float pmp = ws.pm[p];
     const float cbest = pmp + 0.5f * (llrabs - M1);
-    float tau = cbest;
-#pragma unroll
-    for (int off = C::LPP; off < 32; off <<= 1) tau = fmaxf(tau, __shfl_xor_sync(kFull, tau, off));
+    const float tau = key_float(__reduce_max_sync(kFull, float_key(cbest)));
     // |w| >= theta is implied by pm(|w|) <= tau (with slack for rounding)
     const float th0 = llrabs - 2.f * (tau - pmp);
     const float theta = th0 - (fabsf(th0) + llrabs + fabsf(tau) + fabsf(pmp)) * 9.5367431640625e-07f - 1e-30f;
@@ -370,15 +391,8 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
     for (int k = 0; k < V; k++)
         if (fabsf(w[k]) >= theta) mask |= (MaskT)1 << k;
     if (!act) mask = 0;
-    // compaction of candidates into the warp list
     const int cnt = sizeof(MaskT) == 8 ? __popcll((u64)mask) : __popc((u32)mask);
-    int incl = cnt;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const int t = __shfl_up_sync(kFull, incl, off);
-        if (lane >= off) incl += t;
-    }
-    const int total = __shfl_sync(kFull, incl, 31);
+    const int total = __reduce_add_sync(kFull, cnt);
     // spill the transform for candidate extraction (conflict-free STS.128)
     if constexpr (V >= 4) {
 #pragma unroll
@@ -389,15 +403,15 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
         for (int k = 0; k < V; k++) ws.wsp[lane][k] = w[k];
     }
     __syncwarp();
-    // candidates per path (for the per-path top-K rule, fht_decode.py:116)
-    int pcnt = cnt;
-#pragma unroll
-    for (int off = 1; off < LV::act; off <<= 1) pcnt += __shfl_xor_sync(kFull, pcnt, off);
-    if (__all_sync(kFull, pcnt == 1)) {
-        // common case: every path's only candidate is its maximum, so the
-        // pool is the L path maxima ordered by (pm, source slot) (:116-120)
-        const u32 bal = __ballot_sync(kFull, cnt > 0);
-        const int owner = __ffs((bal >> (p * C::LPP)) & ((LV::act >= 32) ? 0xffffffffu : ((1u << LV::act) - 1u))) - 1;
+    RMFHT_STAT(SS * 8 + 0);
+    RMFHT_STAT_ADD(SS * 8 + 4, total);
+    // common case: L candidates in all and every path has one (its maximum is
+    // always a candidate), i.e. every path's only candidate is its maximum
+    const u32 bal = __ballot_sync(kFull, cnt > 0);
+    if (total == L && __all_sync(kFull, ((bal >> (p * C::LPP)) & GBITS) != 0u)) {
+        RMFHT_STAT(SS * 8 + 1);
+        // the pool is the L path maxima ordered by (pm, source slot) (:116-120)
+        const int owner = __ffs((bal >> (p * C::LPP)) & GBITS) - 1;
         int mybin = 0;
         float myw = 0.f;
         if (cnt > 0) {
@@ -420,8 +434,22 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
             ws.sel_pm[rank] = cbest;
         }
         __syncwarp();
-    } else if (total <= kCap) {
+    } else {
+    // candidates per path (for the per-path top-K rule, fht_decode.py:116) and
+    // each lane's position in the warp list (inclusive prefix sum)
+    int pcnt = cnt;
+#pragma unroll
+    for (int off = 1; off < LV::act; off <<= 1) pcnt += __shfl_xor_sync(kFull, pcnt, off);
+    int incl = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(kFull, incl, off);
+        if (lane >= off) incl += t;
+    }
+    if (total <= kCap) {
         const bool over = __any_sync(kFull, pcnt > K);
+        RMFHT_STAT(SS * 8 + 2);
+        if (over) RMFHT_STAT(SS * 8 + 5);
         int pos = incl - cnt;
         // this path's candidates occupy [pstart, pstart + pcnt) (lane order)
         const int pstart = __shfl_sync(kFull, incl - cnt, p * C::LPP);
@@ -501,7 +529,9 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
         }
         __syncwarp();
     } else {
+        RMFHT_STAT(SS * 8 + 3);
         fht_fallback<R, MM, L, SS>(&cx.ws, lane, llrabs);
+    }
     }
     // survivors: pm, lineage; my group's codeword bits
     if (lane < L) {
@@ -1208,6 +1238,9 @@ __global__ void __launch_bounds__(512, 1) decode_kernel2(rmfht::Params<float> pr
     for (long long base = (long long)blockIdx.x * nwarps; base < items; base += stride) {
         const long long item = base + warp;
         if (item < items) {
+#ifdef RMFHT_STATS
+            const long long t_item = clock64();
+#endif
             cp_async_wait_all();
             __syncwarp();
             prefetch_recs(item + stride, cur ^ 1);
@@ -1258,6 +1291,17 @@ __global__ void __launch_bounds__(512, 1) decode_kernel2(rmfht::Params<float> pr
             if (cx.p == best) bitsout[(size_t)item * C::LPP + cx.u] = bits;
             __syncwarp();
             cur ^= 1;
+#ifdef RMFHT_STATS
+            {
+                const long long dt = clock64() - t_item;
+                RMFHT_STAT_ADD(200, dt);
+                RMFHT_STAT_ADD(201, dt * dt / 1024);
+                RMFHT_STAT(202);
+                if (lane_id() == 0) atomicMax(&g_stats[203], (unsigned long long)dt);
+                const int bucket = dt < 2048 ? 0 : dt < 65536 ? 1 + (int)((dt - 2048) / 2048) : 33;
+                RMFHT_STAT(210 + bucket);
+            }
+#endif
         }
         // lock-step rounds: warps share the instruction stream (named barrier per group)
         const int grp = (prm.tie_fix >> 8) & 0xff;  // warps per lock-step group, 0 = none
