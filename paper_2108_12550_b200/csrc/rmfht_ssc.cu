@@ -270,6 +270,61 @@ __global__ void __launch_bounds__(256) aut_ssc_kernel(rmfht::Params<T> prm, int 
     }
 }
 
+}  // namespace rmfht_ssc
+
+#include "rmfht_ssc_reg.cuh"
+
+// compiled register-resident shapes (r, m): the paper's Table IV comparators
+// (RM(2,8), (3,8), (4,8), (2,9)) and the FER / bench shapes
+#define RMFHT_SSC_SHAPES(X) X(2, 9) X(2, 8) X(3, 8) X(4, 8) X(2, 7) X(3, 7) X(2, 6) X(2, 10) X(3, 10) X(2, 5)
+
+namespace rmfht_ssc {
+
+template <typename T, int R, int MM>
+int prepare_reg(rmfht_plan* p) {
+    int nw = 8;
+    const size_t smem = reg_smem_bytes<T, MM>(nw);
+    auto kern = aut_ssc_reg_kernel<T, R, MM>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(RMFHT_ECUDA, std::string("smem attribute: ") + cudaGetErrorString(e));
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem);
+    if (e != cudaSuccess || per_sm < 1) return fail(RMFHT_ECUDA, "Aut-SSC kernel does not fit an SM");
+    p->nwarps = nw;
+    p->smem = smem;
+    p->grid = sms * per_sm;
+    return 0;
+}
+
+template <typename T, int R, int MM>
+int launch_reg(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint32_t* cw, void* pm, int32_t* att,
+               int32_t* path, void* att_pm, uint32_t* att_cw, long long B, cudaStream_t st) {
+    rmfht::Params<T> prm;
+    prm.llr = static_cast<const T*>(llr);
+    prm.maps = maps;
+    prm.B = B;
+    prm.M = p->M;
+    prm.perms = 1;
+    prm.tie_fix = 0;
+    prm.cw = cw;
+    prm.pm = static_cast<T*>(pm);
+    prm.attempt = att;
+    prm.path = path;
+    prm.att_pm = static_cast<T*>(att_pm);
+    prm.att_cw = att_cw;
+    if (B <= 0) return 0;
+    auto* mp = const_cast<rmfht_plan*>(p);
+    std::call_once(mp->once, [mp] { mp->prepared_rc = mp->prepare(mp); });
+    if (p->prepared_rc != 0) return p->prepared_rc;
+    const long long grid = B < p->grid ? B : p->grid;
+    aut_ssc_reg_kernel<T, R, MM><<<(unsigned)grid, p->nwarps * 32, p->smem, st>>>(prm);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(RMFHT_ECUDA, std::string("Aut-SSC launch: ") + cudaGetErrorString(e));
+    return 0;
+}
+
 template <typename T>
 int prepare(rmfht_plan* p) {
     int nw = p->M < 8 ? p->M : 8;
@@ -324,6 +379,18 @@ int rmfht_bind_aut_ssc(rmfht_plan* p) {
     if (p->m > rmfht_ssc::kMaxM) return RMFHT_EUNSUPPORTED;
     p->fast = 0;
     p->generic = 0;
+    if (!p->force_generic) {
+        const bool f64 = p->dtype == RMFHT_F64;
+#define X(R_, M_)                                                                              \
+        if (p->r == R_ && p->m == M_) {                                                         \
+            p->launch = f64 ? &rmfht_ssc::launch_reg<double, R_, M_> : &rmfht_ssc::launch_reg<float, R_, M_>; \
+            p->prepare = f64 ? &rmfht_ssc::prepare_reg<double, R_, M_> : &rmfht_ssc::prepare_reg<float, R_, M_>; \
+            return 0;                                                                           \
+        }
+        RMFHT_SSC_SHAPES(X)
+#undef X
+    }
+    p->generic = 1;  // runtime-shaped shared-memory walk
     if (p->dtype == RMFHT_F64) {
         p->launch = &rmfht_ssc::launch<double>;
         p->prepare = &rmfht_ssc::prepare<double>;

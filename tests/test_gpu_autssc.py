@@ -92,3 +92,23 @@ def test_odd_P_and_warp_counts(oracle_mod, P):
     o = plan.decode(llr.astype(np.float64), records=rec)
     ref = oracle_mod.aut_ssc(3, 7, P, llr.astype(np.float64), raw[:, :, 0, :])
     assert np.array_equal(o["cw"], ref["cw"]) and np.array_equal(o["attempt"], ref["winner"])
+
+
+@pytest.mark.parametrize("r,m,P", [(2, 9, 40), (3, 8, 24), (4, 8, 16), (2, 10, 8), (2, 6, 33), (2, 5, 7)])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_register_kernel_matches_shared_memory_kernel(r, m, P, dtype):
+    """The compiled register-resident kernel (rmfht_ssc_reg.cuh) and the
+    runtime-shaped shared-memory walk give identical results, every decode."""
+    from paper_2108_12550_b200.channel_model import synthetic_frames
+    from paper_2108_12550_b200.decoder import Plan
+    from paper_2108_12550_b200.rm_core import build_code
+    spec = build_code(r, m)
+    _, llr = synthetic_frames(spec, 2.0, 48, seed=r * 100 + m)
+    llr = llr.astype(np.float64 if dtype == "f64" else np.float32)
+    reg = Plan(r, m, 1, P, True, dtype, aut_ssc=True)
+    gen = Plan(r, m, 1, P, True, dtype, aut_ssc=True, generic=True)
+    _, rec = reg.sample(48, seed=P, identity_root=False)
+    a = reg.decode(llr, records=rec, diag=True)
+    b = gen.decode(llr, records=rec, diag=True)
+    for k in ("cw", "pm", "attempt", "att_pm", "att_cw"):
+        assert np.array_equal(a[k], b[k]), k
