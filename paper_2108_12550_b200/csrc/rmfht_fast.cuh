@@ -374,9 +374,18 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
     // (a warp-wide maximum: one REDUX on order-preserving integer keys; cbest
     // can be a rounding error below zero, llrabs and M1 being summed in
     // different orders)
-    float mx = act ? fabsf(w[0]) : -1.f;
+    // (maxima and masks as trees, not V-long dependency chains)
+    float mx;
+    {
+        float t[V];
 #pragma unroll
-    for (int k = 1; k < V; k++) mx = fmaxf(mx, fabsf(w[k]));
+        for (int k = 0; k < V; k++) t[k] = fabsf(w[k]);
+#pragma unroll
+        for (int sd = 1; sd < V; sd <<= 1)
+#pragma unroll
+            for (int k = 0; k + sd < V; k += 2 * sd) t[k] = fmaxf(t[k], t[k + sd]);
+        mx = act ? t[0] : -1.f;
+    }
     constexpr u32 GBITS = (LV::act >= 32) ? 0xffffffffu : ((1u << LV::act) - 1u);  // active lanes of a group
     const float M1 = group_max<LV::act>(mx);
     const float pmp = ws.pm[p];
@@ -386,11 +395,17 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
     const float th0 = llrabs - 2.f * (tau - pmp);
     const float theta = th0 - (fabsf(th0) + llrabs + fabsf(tau) + fabsf(pmp)) * 9.5367431640625e-07f - 1e-30f;
     using MaskT = typename std::conditional<(V > 32), u64, u32>::type;
-    MaskT mask = 0;
+    MaskT mask;
+    {
+        MaskT t[V];
 #pragma unroll
-    for (int k = 0; k < V; k++)
-        if (fabsf(w[k]) >= theta) mask |= (MaskT)1 << k;
-    if (!act) mask = 0;
+        for (int k = 0; k < V; k++) t[k] = fabsf(w[k]) >= theta ? ((MaskT)1 << k) : (MaskT)0;
+#pragma unroll
+        for (int sd = 1; sd < V; sd <<= 1)
+#pragma unroll
+            for (int k = 0; k + sd < V; k += 2 * sd) t[k] |= t[k + sd];
+        mask = act ? t[0] : (MaskT)0;
+    }
     const int cnt = sizeof(MaskT) == 8 ? __popcll((u64)mask) : __popc((u32)mask);
     const int total = __reduce_add_sync(kFull, cnt);
     // spill the transform for candidate extraction (conflict-free STS.128)

@@ -11,11 +11,13 @@ rows = list(csv.reader(out.splitlines()))
 h = rows[1]
 iA, iS, iE = h.index("Address"), h.index("Source"), h.index("Instructions Executed")
 iW = h.index("Warp Stall Sampling (All Samples)")
-metric = os.environ.get("NCU_LINES_METRIC", "exec")
+metric = os.environ.get("NCU_LINES_METRIC", "exec")  # exec | stall | wave | excess
+iX = {"wave": h.index("L1 Wavefronts Shared"), "excess": h.index("L1 Wavefronts Shared Excessive")}.get(metric)
 execs = []
 for r in rows[2:]:
     if len(r) > iE and r[iA].startswith("0x"):
-        val = int(r[iE] or 0) if metric == "exec" else int(r[iW] or 0)
+        col = iE if metric == "exec" else iW if metric == "stall" else iX
+        val = int(float(r[col] or 0))
         execs.append((int(r[iA], 16), r[iS].strip(), val))
 base = execs[0][0]
 sys.path.insert(0, os.path.dirname(__file__))

@@ -43,7 +43,8 @@ _src, _funcs = {}, {}
 
 def source(f):
     if f not in _src:
-        p = glob.glob("/root/repo/**/" + f, recursive=True)
+        root = os.environ.get("SRC_ROOT", "/root/repo")
+        p = glob.glob(root + "/**/" + f, recursive=True)
         _src[f] = open(p[0]).read().split("\n") if p else []
     return _src[f]
 
