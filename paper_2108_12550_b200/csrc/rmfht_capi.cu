@@ -138,7 +138,7 @@ int rmfht_plan_create(int r, int m, int L, int M, int flags, int dtype, rmfht_pl
     p->dtype = dtype;
     p->tie_fix = dtype == RMFHT_F32 ? 1 : 0;
     p->fast = (dtype == RMFHT_F32 && !(flags & RMFHT_REFERENCE_ORDER)) ? 1 : 0;
-    p->lockstep = (flags & RMFHT_NO_LOCKSTEP) ? 0 : 16;
+    p->lockstep = (flags & RMFHT_NO_LOCKSTEP) ? 0 : 255;  // 255: one barrier for the whole CTA
     p->force_generic = (flags & RMFHT_GENERIC) ? 1 : 0;
     if (flags & RMFHT_LOCKSTEP_4) p->lockstep = 4;
     if (flags & RMFHT_LOCKSTEP_8) p->lockstep = 8;

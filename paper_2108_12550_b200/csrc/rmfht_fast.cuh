@@ -95,27 +95,44 @@ struct Lv {
     static constexpr int act = full ? LPP : n;    // active lanes of the group
 };
 
+// an affine map in device-record layout (rmfht.h): columns of A, b, columns
+// of A^-1, A^-1 b — read in place from the item's record buffer
+template <int MM>
+struct MapR {
+    uint16_t col[MM];
+    uint16_t b;
+    uint16_t icol[MM];
+    uint16_t c;
+};
+
+// the throughput kernel's CTA: up to 20 warps (registers capped at 96 by the
+// launch bound; prepare_fast picks the largest multiple of 4 warps whose
+// scratch fits in shared memory)
+constexpr int kFastThreads = 640;
+
 // per-warp shared scratch
 template <int R, int MM, int L>
 struct alignas(16) WS2 {
     using C = Cfg<R, MM, L>;
     static constexpr int RECW = (C::S > 0 ? C::S : 1) * (2 * MM + 2);  // uint16 per item's map records
-    alignas(16) uint16_t recs[2][(RECW + 7) & ~7];  // double-buffered (cp.async prefetch)
-    float lmp[2 * L][32];       // LM lane partials per trial
-    MapS maps[C::S > 0 ? C::S : 1];
-    MapS comp[L];     // composite map of each root path (root perm-ext winners)
-    MapS ctmp[L];
-    MapS bestmap;
-    float pm[L], llrabs[L], pmtmp[2 * L];
+    alignas(16) uint16_t recs[2][(RECW + 7) & ~7];  // double-buffered (cp.async prefetch); the item's maps
+    MapR<MM> comp[L];  // composite map of each root path (root perm-ext winners)
+    MapR<MM> ctmp[L];
+    float pm[L], llrabs[L];
     float lm[2 * L];
     static constexpr int CA = kCap > L * L ? kCap : L * L;  // candidate list (and the exact fallback)
     float ca[CA], cw[CA], cpm[CA];
     int cb[CA], cp[CA], celig[CA];
     alignas(16) u64 ckey[kCap + 4];
     // FHT outputs spilled for candidate extraction: lane-major, padded (conflict-free STS.128)
-    // largest FHT node: RM(1, m-r+1), the first left descendant (the root when r == 1)
+    // largest FHT node: RM(1, m-r+1), the first left descendant (the root when r == 1).
+    // The LM lane partials of the root permutation extension share the space
+    // (they are dead before the first FHT node).
     static constexpr int VMAX = cmax(4, (R == 1 ? C::N : (C::N >> (R - 1))) / C::LPP);
-    alignas(16) float wsp[32][VMAX + 4];
+    union alignas(16) {
+        float wsp[32][VMAX + 4];
+        float lmp[2 * L][32];
+    };
     int sel_src[2 * L], sel_bin[2 * L];
     float sel_w[2 * L], sel_pm[2 * L];
     int8_t l0[MM + 1][L], l1[MM + 1][L], l2[MM + 1][L], rootchain[L], ord[2 * L];
@@ -126,10 +143,7 @@ struct alignas(16) WS2 {
     uint16_t sord[L * 16];
     float vbuf[R >= 3 ? L * C::N : 1];  // inner permutation nodes
     uint8_t ubits[R >= 3 ? L * C::N : 1];
-    uint32_t bestbits[C::N / 32];  // best codeword of this warp (channel domain)
-    uint32_t scrbits[C::N / 32];   // scratch: a path's bits in the permuted domain
-    float best_pm;
-    int best_att, best_path, next_map, ncand, spc_cnt;
+    int next_map;
 };
 
 template <int R, int MM, int L>
@@ -137,6 +151,7 @@ struct Ctx2 {
     using C = Cfg<R, MM, L>;
     WS2<R, MM, L>& ws;
     const float* alpha;        // frame LLRs (shared memory)
+    const MapR<MM>* maps;      // the item's map records (shared memory)
     float ach[C::NS];          // channel layout: ach[s] = alpha[lane + 32 s]
     int lane, p, u;
     u32 alpha_saddr;           // shared-window address of alpha (2 KB aligned)
@@ -158,6 +173,14 @@ __device__ __forceinline__ u32 float_key(float f) {
 }
 __device__ __forceinline__ float key_float(u32 k) {
     return __uint_as_float(k ^ ((k >> 31) ? 0x80000000u : 0xffffffffu));
+}
+
+template <int MN>
+__device__ __forceinline__ u32 lin_apply(const uint16_t* cols, u32 x) {
+    u32 v = 0;
+#pragma unroll
+    for (int k = 0; k < MN; k++) v ^= (x >> k & 1u) ? (u32)cols[k] : 0u;
+    return v;
 }
 
 // group-local xor reduce / broadcast helpers
@@ -184,23 +207,24 @@ struct RootIdx {
     u32 base, A[NA], B[NB];
     // alpha_saddr: shared-window address of the frame LLRs, aligned to 2 KB so
     // that XOR-ing byte offsets (< 2 KB) into it forms the address directly
-    __device__ __forceinline__ void build(const MapS& mp, int u, u32 alpha_saddr) {
+    template <typename Map>
+    __device__ __forceinline__ void build(const Map& mp, int u, u32 alpha_saddr) {
         constexpr int LB = clog2(LPP);
         u32 bse = mp.c;
 #pragma unroll
-        for (int b = 0; b < LB; b++) bse ^= (u >> b & 1) ? mp.icol[b] : 0u;
+        for (int b = 0; b < LB; b++) bse ^= (u >> b & 1) ? (u32)mp.icol[b] : 0u;
         base = alpha_saddr | (bse << 2);
         A[0] = 0;
 #pragma unroll
         for (int i = 1; i < NA; i++) {
             const int b = __ffs(i) - 1;  // lowest set bit: A[i] = A[i & (i-1)] ^ col
-            A[i] = A[i & (i - 1)] ^ (mp.icol[LB + b] << 2);
+            A[i] = A[i & (i - 1)] ^ ((u32)mp.icol[LB + b] << 2);
         }
         B[0] = 0;
 #pragma unroll
         for (int i = 1; i < NB; i++) {
             const int b = __ffs(i) - 1;
-            B[i] = B[i & (i - 1)] ^ (mp.icol[LB + clog2(NA) + b] << 2);
+            B[i] = B[i & (i - 1)] ^ ((u32)mp.icol[LB + clog2(NA) + b] << 2);
         }
     }
     __device__ __forceinline__ u32 off(int k) const { return base ^ A[k % NA] ^ B[k / NA]; }
@@ -909,7 +933,7 @@ __device__ __forceinline__ void perm_ext_root2(Ctx2<R, MM, L>& cx) {
     const int lane = cx.lane, base = ws.next_map;
     // pairing direction of each trial's composite: A_init^-1 (A_t^-1 e_{m-1})
     if (lane < 2 * L) {
-        const u32 d = lin_apply<MM>(ws.comp[lane % L].icol, ws.maps[base + lane].icol[MM - 1]);
+        const u32 d = lin_apply<MM>(ws.comp[lane % L].icol, (u32)cx.maps[base + lane].icol[MM - 1]);
         ws.cb[lane] = (int)d;
     }
     __syncwarp();
@@ -928,10 +952,10 @@ __device__ __forceinline__ void perm_ext_root2(Ctx2<R, MM, L>& cx) {
     for (int task = lane; task < L * (MM + 1); task += 32) {
         const int o = task / (MM + 1), k = task % (MM + 1);
         const int t = ws.ord[o];
-        const MapS& tm = ws.maps[base + t];
-        const MapS& im = ws.comp[t % L];
-        if (k < MM) ws.ctmp[o].icol[k] = lin_apply<MM>(im.icol, tm.icol[k]);
-        else ws.ctmp[o].c = lin_apply<MM>(im.icol, tm.c) ^ im.c;
+        const MapR<MM>& tm = cx.maps[base + t];
+        const MapR<MM>& im = ws.comp[t % L];
+        if (k < MM) ws.ctmp[o].icol[k] = (uint16_t)lin_apply<MM>(im.icol, (u32)tm.icol[k]);
+        else ws.ctmp[o].c = (uint16_t)(lin_apply<MM>(im.icol, (u32)tm.c) ^ im.c);
     }
     float npm = 0.f;
     if (lane < L) npm = ws.pm[ws.ord[lane] % L];
@@ -963,7 +987,7 @@ __device__ __forceinline__ void perm_ext_inner2(Ctx2<R, MM, L>& cx, float (&x)[L
         const int e = LV::full ? k * C::LPP + u : u;
         if (LV::full || u < n) ws.vbuf[p * n + e] = x[k];
     }
-    if (lane < 2 * L) ws.cb[lane] = (int)ws.maps[base + lane].icol[SS - 1];
+    if (lane < 2 * L) ws.cb[lane] = (int)cx.maps[base + lane].icol[SS - 1];
     __syncwarp();
     float part[2 * L];
 #pragma unroll
@@ -988,11 +1012,11 @@ __device__ __forceinline__ void perm_ext_inner2(Ctx2<R, MM, L>& cx, float (&x)[L
     // winners: permuted vectors x'[j] = x_src[sigma^-1(j)]
     const int t = ws.ord[p];
     const int src = t % L;
-    const MapS& mp = ws.maps[base + t];
+    const MapR<MM>& mp = cx.maps[base + t];
 #pragma unroll
     for (int k = 0; k < V; k++) {
         const int e = LV::full ? k * C::LPP + u : u;
-        const u32 j = mp.c ^ lin_apply<SS>(mp.icol, (u32)e);
+        const u32 j = (u32)mp.c ^ lin_apply<SS>(mp.icol, (u32)e);
         x[k] = (LV::full || u < n) ? ws.vbuf[src * n + j] : 0.f;
     }
     float npm = 0.f;
@@ -1117,12 +1141,12 @@ __device__ __forceinline__ u64 node2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / 
                 if (LV::full || u < n) ws.ubits[p * n + e] = (uint8_t)((out >> k) & 1ull);
             }
             __syncwarp();
-            const MapS& mp = ws.maps[ws.nmap[SS][chain]];
+            const MapR<MM>& mp = cx.maps[ws.nmap[SS][chain]];
             u64 o2 = 0;
 #pragma unroll
             for (int k = 0; k < V; k++) {
                 const int e = LV::full ? k * C::LPP + u : u;
-                const u32 sidx = mp.b ^ lin_apply<SS>(mp.col, (u32)e);
+                const u32 sidx = (u32)mp.b ^ lin_apply<SS>(mp.col, (u32)e);
                 if (LV::full || u < n) o2 |= (u64)ws.ubits[p * n + sidx] << k;
             }
             out = o2;
@@ -1209,7 +1233,7 @@ struct AttHdr {
 // lock-stepped rounds (they run the same code path, so they share the
 // instruction stream).
 template <int R, int MM, int L>
-__global__ void __launch_bounds__(512, 1) decode_kernel2(rmfht::Params<float> prm, AttHdr* hdr, u64* bitsout) {
+__global__ void __launch_bounds__(kFastThreads, 1) decode_kernel2(rmfht::Params<float> prm, AttHdr* hdr, u64* bitsout) {
     using C = Cfg<R, MM, L>;
     using WS = WS2<R, MM, L>;
     using LV = Lv<MM, C::LPP>;
@@ -1225,7 +1249,8 @@ __global__ void __launch_bounds__(512, 1) decode_kernel2(rmfht::Params<float> pr
     WS* wsarr = reinterpret_cast<WS*>(smem_raw + pad + (size_t)nwarps * ASTRIDE);
     WS& ws = wsarr[warp];
     const u32 asa = (u32)__cvta_generic_to_shared(alpha_w);
-    Ctx2<R, MM, L> cx{ws, alpha_w, {}, lane, lane / C::LPP, lane % C::LPP, asa};
+    Ctx2<R, MM, L> cx{ws, alpha_w, nullptr, {}, lane, lane / C::LPP, lane % C::LPP, asa};
+    static_assert(sizeof(MapR<MM>) == 2 * (2 * MM + 2), "record layout");
     constexpr bool ROOT_INTERNAL = !(R == 1 || R == MM - 1);
     const long long items = prm.B * (long long)prm.M;
     const long long stride = (long long)gridDim.x * nwarps;
@@ -1261,14 +1286,9 @@ __global__ void __launch_bounds__(512, 1) decode_kernel2(rmfht::Params<float> pr
             prefetch_recs(item + stride, cur ^ 1);
 #pragma unroll
             for (int s = 0; s < C::NS; s++) cx.ach[s] = alpha_w[lane + 32 * s];
-            const uint16_t* recs = ws.recs[cur];
-            for (int s = lane; s < S; s += 32) {
-                const int mn = s < L ? MM : MM - (s - L) / (2 * L);
-                rmfht::load_map(ws.maps[s], recs + (size_t)s * REC, MM, mn);
-            }
-            __syncwarp();
+            cx.maps = reinterpret_cast<const MapR<MM>*>(ws.recs[cur]);
             if (lane < L) {
-                ws.comp[lane] = ws.maps[lane];  // L root maps (:129-139)
+                ws.comp[lane] = cx.maps[lane];  // L root maps (:129-139)
                 ws.pm[lane] = 0.f;
                 ws.l0[MM][lane] = (int8_t)lane;
                 ws.nmap[MM][lane] = -1;
@@ -1320,7 +1340,7 @@ __global__ void __launch_bounds__(512, 1) decode_kernel2(rmfht::Params<float> pr
         }
         // lock-step rounds: warps share the instruction stream (named barrier per group)
         const int grp = (prm.tie_fix >> 8) & 0xff;  // warps per lock-step group, 0 = none
-        if (grp >= nwarps) {
+        if (grp >= nwarps || nwarps % grp != 0) {
             __syncthreads();
         } else if (grp > 0) {
             asm volatile("bar.sync %0, %1;" ::"r"(1 + warp / grp), "r"(grp * 32) : "memory");

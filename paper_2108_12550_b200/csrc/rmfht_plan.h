@@ -16,7 +16,7 @@ using PrepareFn = int (*)(rmfht_plan*);
 
 struct rmfht_plan {
     int r, m, L, M, perms, tie_fix, dtype;
-    int lockstep = 16;  // throughput kernel: warps per lock-step group (0 = none)
+    int lockstep = 255;  // throughput kernel: warps per lock-step group (0 = none, >= CTA warps = whole CTA)
     int fast;  // float32 throughput kernel (rmfht_fast.cuh) instead of the reference-order one
     int generic = 0;  // runtime-shaped interpreter kernel (rmfht_generic.cuh)
     int force_generic = 0;
