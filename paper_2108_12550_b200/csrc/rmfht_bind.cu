@@ -114,7 +114,7 @@ int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
 
 template <int R, int MM, int L>
 int prepare_fast(rmfht_plan* p) {
-    int nw = rmfht2::kFastThreads / 32;
+    int nw = rmfht2::fast_warps<R, MM, L>();
     while (nw > 4 && rmfht2::smem_bytes2<R, MM, L>(nw) > 227 * 1024) nw -= 4;  // 227 KB: the sm_100 opt-in maximum
     const size_t smem = rmfht2::smem_bytes2<R, MM, L>(nw);
     auto kern = rmfht2::decode_kernel2<R, MM, L>;

@@ -105,11 +105,6 @@ struct MapR {
     uint16_t c;
 };
 
-// the throughput kernel's CTA: up to 20 warps (registers capped at 96 by the
-// launch bound; prepare_fast picks the largest multiple of 4 warps whose
-// scratch fits in shared memory)
-constexpr int kFastThreads = 640;
-
 // per-warp shared scratch
 template <int R, int MM, int L>
 struct alignas(16) WS2 {
@@ -1228,12 +1223,27 @@ struct AttHdr {
     int path, init_map, trial_map;
 };
 
+template <int R, int MM, int L>
+constexpr size_t smem_bytes2(int nwarps) {
+    // 2 KB alignment pad + per-warp LLR copy (N floats, N-aligned) + per-warp scratch
+    return 2048 + size_t(1 << MM) * 4 * size_t(nwarps) + sizeof(WS2<R, MM, L>) * size_t(nwarps);
+}
+
+// warps per CTA: the largest multiple of 4 (at most 24, i.e. an 80-register
+// cap) whose LLR copies and scratch fit in 227 KB of shared memory
+template <int R, int MM, int L>
+constexpr int fast_warps() {
+    int w = 24;
+    while (w > 4 && smem_bytes2<R, MM, L>(w) > 227 * 1024) w -= 4;
+    return w;
+}
+
 // ------------------------------------------------------------- kernel ----
 // Work item = (frame, attempt); warps of a CTA take consecutive items in
 // lock-stepped rounds (they run the same code path, so they share the
 // instruction stream).
 template <int R, int MM, int L>
-__global__ void __launch_bounds__(kFastThreads, 1) decode_kernel2(rmfht::Params<float> prm, AttHdr* hdr, u64* bitsout) {
+__global__ void __launch_bounds__(32 * fast_warps<R, MM, L>(), 1) decode_kernel2(rmfht::Params<float> prm, AttHdr* hdr, u64* bitsout) {
     using C = Cfg<R, MM, L>;
     using WS = WS2<R, MM, L>;
     using LV = Lv<MM, C::LPP>;
@@ -1244,7 +1254,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) decode_kernel2(rmfht::Params<
     // per-warp frame LLRs, each 2 KB aligned in the shared window, then the scratch
     const u32 raw_saddr = (u32)__cvta_generic_to_shared(smem_raw);
     const u32 pad = ((raw_saddr + 2047u) & ~2047u) - raw_saddr;
-    constexpr u32 ASTRIDE = ((u32)N * 4u + 2047u) & ~2047u;
+    constexpr u32 ASTRIDE = (u32)N * 4u;  // N-aligned: gather offsets (< 4N bytes) are OR-ed into the base
     float* const alpha_w = reinterpret_cast<float*>(smem_raw + pad + (size_t)warp * ASTRIDE);
     WS* wsarr = reinterpret_cast<WS*>(smem_raw + pad + (size_t)nwarps * ASTRIDE);
     WS& ws = wsarr[warp];
@@ -1420,12 +1430,6 @@ __global__ void __launch_bounds__(256) reduce_kernel2(rmfht::Params<float> prm, 
     }
 }
 
-template <int R, int MM, int L>
-constexpr size_t smem_bytes2(int nwarps) {
-    // 2 KB alignment pad + per-warp LLR copy + per-warp scratch
-    return 2048 + ((size_t(1 << MM) * 4 + 2047) & ~size_t(2047)) * size_t(nwarps) +
-           sizeof(WS2<R, MM, L>) * size_t(nwarps);
-}
 
 template <int R, int MM, int L>
 constexpr size_t work_bytes2() {
