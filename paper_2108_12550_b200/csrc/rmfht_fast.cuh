@@ -112,12 +112,12 @@ struct alignas(16) WS2 {
     static constexpr int RECW = (C::S > 0 ? C::S : 1) * (2 * MM + 2);  // uint16 per item's map records
     alignas(16) uint16_t recs[2][(RECW + 7) & ~7];  // double-buffered (cp.async prefetch); the item's maps
     MapR<MM> comp[L];  // composite map of each root path (root perm-ext winners)
-    MapR<MM> ctmp[L];
     float pm[L], llrabs[L];
     float lm[2 * L];
     static constexpr int CA = kCap > L * L ? kCap : L * L;  // candidate list (and the exact fallback)
-    float ca[CA], cw[CA], cpm[CA];
-    int cb[CA], cp[CA], celig[CA];
+    static constexpr int CB = L * L > 2 * L ? L * L : 2 * L;  // per path / per split / fallback pool
+    float ca[CA], cw[CA], cpm[CB];
+    int cb[CB], cp[CB], celig[CB];
     alignas(16) u64 ckey[kCap + 4];
     // FHT outputs spilled for candidate extraction: lane-major, padded (conflict-free STS.128)
     // largest FHT node: RM(1, m-r+1), the first left descendant (the root when r == 1).
@@ -125,9 +125,16 @@ struct alignas(16) WS2 {
     // (they are dead before the first FHT node).
     static constexpr int VMAX = cmax(4, (R == 1 ? C::N : (C::N >> (R - 1))) / C::LPP);
     union alignas(16) {
-        float wsp[32][VMAX + 4];
+        float wsp[32][VMAX];  // 16-byte chunks XOR-swizzled per lane (wsp_idx): conflict-free STS.128
         float lmp[2 * L][32];
     };
+    // element k of lane `lane`'s row
+    __device__ __forceinline__ static int wsp_idx(int lane, int k) {
+        constexpr int G = VMAX / 4;  // 16-byte chunks per row
+        const int swz = G >= 8 ? (lane & 7) : ((lane / (8 / G)) & (G - 1));
+        return (((k >> 2) ^ swz) << 2) | (k & 3);
+    }
+    __device__ __forceinline__ float& wspk(int lane, int k) { return wsp[lane][wsp_idx(lane, k)]; }
     int sel_src[2 * L], sel_bin[2 * L];
     float sel_w[2 * L], sel_pm[2 * L];
     int8_t l0[MM + 1][L], l1[MM + 1][L], l2[MM + 1][L], rootchain[L], ord[2 * L];
@@ -279,7 +286,7 @@ __device__ __noinline__ void fht_fallback(WS2<R, MM, L>* wsp_, int lane, float l
 #pragma unroll
             for (int k = 0; k < V; k++) {
                 const int e = LV::full ? k * C::LPP + u : u;
-                const float wk = ws.wsp[lane][k];
+                const float wk = ws.wspk(lane, k);
                 const float a = fabsf(wk);
                 if (act && !((taken >> k) & 1ull) && (a > bv || (a == bv && e < bb))) { bv = a; bb = e; bw = wk; }
             }
@@ -431,10 +438,10 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
     if constexpr (V >= 4) {
 #pragma unroll
         for (int k = 0; k < V; k += 4)
-            *reinterpret_cast<float4*>(&ws.wsp[lane][k]) = make_float4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+            *reinterpret_cast<float4*>(&ws.wspk(lane, k)) = make_float4(w[k], w[k + 1], w[k + 2], w[k + 3]);
     } else {
 #pragma unroll
-        for (int k = 0; k < V; k++) ws.wsp[lane][k] = w[k];
+        for (int k = 0; k < V; k++) ws.wspk(lane, k) = w[k];
     }
     __syncwarp();
     RMFHT_STAT(SS * 8 + 0);
@@ -451,7 +458,7 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
         if (cnt > 0) {
             const int k = (sizeof(MaskT) == 8 ? __ffsll((long long)mask) : __ffs((int)mask)) - 1;
             mybin = LV::full ? k * C::LPP + u : u;
-            myw = ws.wsp[lane][k];
+            myw = ws.wspk(lane, k);
         }
         const int bin = __shfl_sync(kFull, mybin, p * C::LPP + owner);
         const float wv = __shfl_sync(kFull, myw, p * C::LPP + owner);
@@ -495,7 +502,7 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
         while (mk) {
             const int k = sizeof(MaskT) == 8 ? __ffsll((long long)mk) - 1 : __ffs((int)mk) - 1;
             mk &= mk - 1;
-            const float v = ws.wsp[lane][k];
+            const float v = ws.wspk(lane, k);
             const float a = fabsf(v);
             const int bin = LV::full ? k * C::LPP + u : u;
             const float pmc = pmp + 0.5f * (llrabs - a);  // :119
@@ -944,21 +951,33 @@ __device__ __forceinline__ void perm_ext_root2(Ctx2<R, MM, L>& cx) {
     __syncwarp();
     select_trials2(cx);
     // composites of the winners (inverse direction), one column per lane task
-    for (int task = lane; task < L * (MM + 1); task += 32) {
-        const int o = task / (MM + 1), k = task % (MM + 1);
-        const int t = ws.ord[o];
-        const MapR<MM>& tm = cx.maps[base + t];
-        const MapR<MM>& im = ws.comp[t % L];
-        if (k < MM) ws.ctmp[o].icol[k] = (uint16_t)lin_apply<MM>(im.icol, (u32)tm.icol[k]);
-        else ws.ctmp[o].c = (uint16_t)(lin_apply<MM>(im.icol, (u32)tm.c) ^ im.c);
+    // (computed into registers, written after every lane has read the old ones)
+    constexpr int NT = (L * (MM + 1) + 31) / 32;
+    uint16_t nv[NT];
+#pragma unroll
+    for (int q = 0; q < NT; q++) {
+        const int task = lane + 32 * q;
+        nv[q] = 0;
+        if (task < L * (MM + 1)) {
+            const int o = task / (MM + 1), k = task % (MM + 1);
+            const int t = ws.ord[o];
+            const MapR<MM>& tm = cx.maps[base + t];
+            const MapR<MM>& im = ws.comp[t % L];
+            nv[q] = k < MM ? (uint16_t)lin_apply<MM>(im.icol, (u32)tm.icol[k])
+                           : (uint16_t)(lin_apply<MM>(im.icol, (u32)tm.c) ^ im.c);
+        }
     }
     float npm = 0.f;
     if (lane < L) npm = ws.pm[ws.ord[lane] % L];
     __syncwarp();
-    for (int task = lane; task < L * (MM + 1); task += 32) {
-        const int o = task / (MM + 1), k = task % (MM + 1);
-        if (k < MM) ws.comp[o].icol[k] = ws.ctmp[o].icol[k];
-        else ws.comp[o].c = ws.ctmp[o].c;
+#pragma unroll
+    for (int q = 0; q < NT; q++) {
+        const int task = lane + 32 * q;
+        if (task < L * (MM + 1)) {
+            const int o = task / (MM + 1), k = task % (MM + 1);
+            if (k < MM) ws.comp[o].icol[k] = nv[q];
+            else ws.comp[o].c = nv[q];
+        }
     }
     if (lane < L) {
         ws.pm[lane] = npm;
