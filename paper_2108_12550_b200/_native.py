@@ -12,7 +12,7 @@ import subprocess
 import sys
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librmfht.so")
+LIB_PATH = os.environ.get("RMFHT_LIB_OVERRIDE") or os.path.join(_HERE, "librmfht.so")  # override: A/B experiments only
 CSRC = os.path.join(_HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(_HERE), "include")
 
