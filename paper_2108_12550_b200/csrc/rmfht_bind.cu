@@ -77,7 +77,7 @@ int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
     prm.maps = maps;
     prm.B = B;
     prm.M = p->M;
-    prm.perms = 1;
+    prm.perms = p->perms;
     prm.tie_fix = (p->lockstep & 0xff) << 8;  // warps per lock-step group (the fast kernel has no tie fix)
     prm.cw = cw;
     prm.pm = static_cast<float*>(pm);
@@ -105,7 +105,11 @@ int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
     auto* bits = reinterpret_cast<unsigned long long*>(static_cast<char*>(mp->work) + items * sizeof(rmfht2::AttHdr));
     const long long blocks_needed = ((long long)items + p->nwarps - 1) / p->nwarps;
     const long long grid = blocks_needed < p->grid ? blocks_needed : p->grid;
-    rmfht2::decode_kernel2<R, MM, L><<<(unsigned)grid, p->nwarps * 32, p->smem, st>>>(prm, hdr, bits);
+    if (p->perms) {
+        rmfht2::decode_kernel2<R, MM, L, true><<<(unsigned)grid, p->nwarps * 32, p->smem, st>>>(prm, hdr, bits);
+    } else if constexpr (L == 1) {
+        rmfht2::decode_kernel2<R, MM, L, false><<<(unsigned)grid, p->nwarps * 32, p->smem, st>>>(prm, hdr, bits);
+    }
     rmfht2::reduce_kernel2<R, MM, L><<<(unsigned)((B + 7) / 8), 256, 0, st>>>(prm, hdr, bits);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(RMFHT_ECUDA, std::string("decode launch: ") + cudaGetErrorString(e));
@@ -117,7 +121,10 @@ int prepare_fast(rmfht_plan* p) {
     int nw = rmfht2::fast_warps<R, MM, L>();
     while (nw > 4 && rmfht2::smem_bytes2<R, MM, L>(nw) > 227 * 1024) nw -= 4;  // 227 KB: the sm_100 opt-in maximum
     const size_t smem = rmfht2::smem_bytes2<R, MM, L>(nw);
-    auto kern = rmfht2::decode_kernel2<R, MM, L>;
+    auto kern = rmfht2::decode_kernel2<R, MM, L, true>;
+    if constexpr (L == 1) {
+        if (!p->perms) kern = rmfht2::decode_kernel2<R, MM, L, false>;
+    }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(RMFHT_ECUDA, std::string("smem attribute: ") + cudaGetErrorString(e));
     int dev = 0, sms = 148, per_sm = 1;
@@ -134,7 +141,10 @@ int prepare_fast(rmfht_plan* p) {
 template <typename T, int R, int MM, int L>
 int bind_one(rmfht_plan* p) {
     if constexpr (sizeof(T) == 4 && (1 << MM) >= 32 && L <= 8) {
-        if (p->fast && p->perms) {
+        // without permutations the list starts from one path and grows, which
+        // the throughput kernel (P == L at every node) does not model: FHT-FSC
+        // (L = 1) only
+        if (p->fast && (p->perms || L == 1)) {
             p->launch = &launch_fast<R, MM, L>;
             p->prepare = &prepare_fast<R, MM, L>;
             return 0;

@@ -153,7 +153,8 @@ struct Ctx2 {
     using C = Cfg<R, MM, L>;
     WS2<R, MM, L>& ws;
     const float* alpha;        // frame LLRs (shared memory)
-    const MapR<MM>* maps;      // the item's map records (shared memory)
+    const MapR<MM>* maps;      // the item's map records (shared memory); unused without permutations
+    int perms;                 // p-FHT-FSCL (else FHT-FSCL / FHT-FSC: identity maps, no permutation nodes)
     float ach[C::NS];          // channel layout: ach[s] = alpha[lane + 32 s]
     int lane, p, u;
     u32 alpha_saddr;           // shared-window address of alpha (2 KB aligned)
@@ -1096,8 +1097,8 @@ __device__ __forceinline__ u64 node2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / 
         int8_t* l0 = ws.l0[SS];
         int8_t* l1 = ws.l1[SS];
         int8_t* l2 = ws.l2[SS];
-        if constexpr (INNER_PERM) {
-            perm_ext_inner2<R, MM, L, SS>(cx, x);
+        if (INNER_PERM && cx.perms) {
+            if constexpr (INNER_PERM) perm_ext_inner2<R, MM, L, SS>(cx, x);
         } else if constexpr (SS < MM) {
             if (lane < L) l0[lane] = (int8_t)lane;
             __syncwarp();
@@ -1147,7 +1148,7 @@ __device__ __forceinline__ u64 node2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / 
             if (!(LV::full || u < n)) out = 0;
         }
         const int chain = l1[src2];
-        if constexpr (INNER_PERM) {
+        if (INNER_PERM && cx.perms) {
             // un-permute by this node's trial map (:109-112): out[i] = beta[sigma(i)]
 #pragma unroll
             for (int k = 0; k < V; k++) {
@@ -1261,7 +1262,8 @@ constexpr int fast_warps() {
 // Work item = (frame, attempt); warps of a CTA take consecutive items in
 // lock-stepped rounds (they run the same code path, so they share the
 // instruction stream).
-template <int R, int MM, int L>
+// PM: permutations (p-FHT-FSCL); false = FHT-FSC (L = 1, identity maps)
+template <int R, int MM, int L, bool PM = true>
 __global__ void __launch_bounds__(32 * fast_warps<R, MM, L>(), 1) decode_kernel2(rmfht::Params<float> prm, AttHdr* hdr, u64* bitsout) {
     using C = Cfg<R, MM, L>;
     using WS = WS2<R, MM, L>;
@@ -1278,7 +1280,7 @@ __global__ void __launch_bounds__(32 * fast_warps<R, MM, L>(), 1) decode_kernel2
     WS* wsarr = reinterpret_cast<WS*>(smem_raw + pad + (size_t)nwarps * ASTRIDE);
     WS& ws = wsarr[warp];
     const u32 asa = (u32)__cvta_generic_to_shared(alpha_w);
-    Ctx2<R, MM, L> cx{ws, alpha_w, nullptr, {}, lane, lane / C::LPP, lane % C::LPP, asa};
+    Ctx2<R, MM, L> cx{ws, alpha_w, nullptr, PM ? 1 : 0, {}, lane, lane / C::LPP, lane % C::LPP, asa};
     static_assert(sizeof(MapR<MM>) == 2 * (2 * MM + 2), "record layout");
     constexpr bool ROOT_INTERNAL = !(R == 1 || R == MM - 1);
     const long long items = prm.B * (long long)prm.M;
@@ -1288,7 +1290,7 @@ __global__ void __launch_bounds__(32 * fast_warps<R, MM, L>(), 1) decode_kernel2
     // as soon as the current item has read the frame LLRs for the last time
     // (after the root's g, i.e. before the right half of the tree).
     auto prefetch_recs = [&](long long it, int buf) {
-        if (it >= items) return;
+        if (it >= items || !PM) return;
         const u32 rsa = (u32)__cvta_generic_to_shared(ws.recs[buf]);
         const char* gr = reinterpret_cast<const char*>(prm.maps + (size_t)it * S * REC);
         for (int i = lane; i < WS::RECW / 2; i += 32) cp_async4(rsa + 4u * i, gr + 4 * i);
@@ -1317,7 +1319,13 @@ __global__ void __launch_bounds__(32 * fast_warps<R, MM, L>(), 1) decode_kernel2
             for (int s = 0; s < C::NS; s++) cx.ach[s] = alpha_w[lane + 32 * s];
             cx.maps = reinterpret_cast<const MapR<MM>*>(ws.recs[cur]);
             if (lane < L) {
-                ws.comp[lane] = cx.maps[lane];  // L root maps (:129-139)
+                if constexpr (PM) {
+                    ws.comp[lane] = cx.maps[lane];  // L root maps (:129-139)
+                } else {
+#pragma unroll
+                    for (int k = 0; k < MM; k++) ws.comp[lane].col[k] = ws.comp[lane].icol[k] = (uint16_t)(1u << k);
+                    ws.comp[lane].b = ws.comp[lane].c = 0;
+                }
                 ws.pm[lane] = 0.f;
                 ws.l0[MM][lane] = (int8_t)lane;
                 ws.nmap[MM][lane] = -1;
@@ -1326,7 +1334,9 @@ __global__ void __launch_bounds__(32 * fast_warps<R, MM, L>(), 1) decode_kernel2
             __syncwarp();
             int8_t* rlin = ws.l2[0];  // root lineage (level-0 slot is unused by nodes)
             u64 bits;
-            if constexpr (ROOT_INTERNAL) perm_ext_root2(cx);
+            if constexpr (ROOT_INTERNAL) {
+                if constexpr (PM) perm_ext_root2(cx);
+            }
             if constexpr (ROOT_INTERNAL && Lv<MM - 1, C::LPP>::full) {
                 bits = root_node(cx, rlin, [&] { prefetch_alpha(item + stride); });
             } else {
@@ -1348,8 +1358,8 @@ __global__ void __launch_bounds__(32 * fast_warps<R, MM, L>(), 1) decode_kernel2
                 AttHdr h;
                 h.pm = ws.pm[best];
                 h.path = best;
-                h.init_map = ROOT_INTERNAL ? ws.l0[MM][rslot] : rslot;
-                h.trial_map = ROOT_INTERNAL ? ws.nmap[MM][rslot] : -1;
+                h.init_map = !PM ? -1 : ROOT_INTERNAL ? ws.l0[MM][rslot] : rslot;
+                h.trial_map = !PM ? -1 : ROOT_INTERNAL ? ws.nmap[MM][rslot] : -1;
                 hdr[item] = h;
             }
             if (cx.p == best) bitsout[(size_t)item * C::LPP + cx.u] = bits;
@@ -1410,7 +1420,12 @@ __global__ void __launch_bounds__(256) reduce_kernel2(rmfht::Params<float> prm, 
         if (lane < LPP) sbits[warp][lane] = bitsin[(size_t)item * LPP + lane];
         if (lane == 0) {
             MapS im, fm;
-            rmfht::load_map(im, prm.maps + ((size_t)item * S + h.init_map) * REC, MM, MM);
+            if (h.init_map < 0) {  // no permutations: identity
+                for (int k = 0; k < rmfht::kMaxM; k++) im.col[k] = im.icol[k] = k < MM ? (1u << k) : 0u;
+                im.b = im.c = 0;
+            } else {
+                rmfht::load_map(im, prm.maps + ((size_t)item * S + h.init_map) * REC, MM, MM);
+            }
             if (h.trial_map >= 0) {
                 MapS tm;
                 rmfht::load_map(tm, prm.maps + ((size_t)item * S + h.trial_map) * REC, MM, MM);
