@@ -27,17 +27,22 @@ namespace rmfht_ssc {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kMaxM = 10;
 
-template <typename T>
-__device__ __forceinline__ T f_op(T a, T b) {  // list_engine.py:15-20
-    const T x = a < T(0) ? -a : a, y = b < T(0) ? -b : b;
-    const T mn = y < x ? y : x;
-    return ((a < T(0)) != (b < T(0))) ? -mn : mn;
+// f_op, list_engine.py:15-20: min(|a|,|b|) sgn(a) sgn(b).  The sign comes from
+// the product's sign bit (MNMX + MUL + LOP3); it differs from sgn(a)sgn(b)
+// (sgn(0) = +1) only on a zero result, where it yields -0.0 == +0.0 — every
+// downstream use is a comparison with 0 or a sum, so results are unchanged.
+__device__ __forceinline__ float f_op(float a, float b) {
+    const float m = fminf(fabsf(a), fabsf(b));
+    return __int_as_float(__float_as_int(m) | (__float_as_int(a * b) & 0x80000000));
+}
+__device__ __forceinline__ double f_op(double a, double b) {
+    const double m = fmin(fabs(a), fabs(b));
+    return __longlong_as_double(__double_as_longlong(m) | (__double_as_longlong(a * b) & (long long)0x8000000000000000ull));
 }
 
-template <typename T>
-__device__ __forceinline__ T g_op(T a, T b, int c) {  // list_engine.py:23-27
-    return c ? b - a : b + a;
-}
+// g_op, list_engine.py:23-27: b + (1 - 2c) a, one rounding (exactly b - a or b + a)
+__device__ __forceinline__ float g_op(float a, float b, int c) { return __fmaf_rn(c ? -1.f : 1.f, a, b); }
+__device__ __forceinline__ double g_op(double a, double b, int c) { return __fma_rn(c ? -1.0 : 1.0, a, b); }
 
 __device__ __forceinline__ unsigned lin(const uint16_t* cols, int m, unsigned x) {
     unsigned v = 0;
