@@ -85,11 +85,13 @@ __device__ __forceinline__ uint32_t ssc_node(const T (&x)[NodeL<S>::V], int lane
             const T v = x[k] < T(0) ? -x[k] : x[k];
             if (act && (be == 0x7fffffff || v < bv)) { bv = v; be = k * 32 + lane; }
         }
+        // argmin over the node's lanes only (log2(min(n, 32)) steps; every
+        // participating lane holds a candidate)
 #pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) {
+        for (int off = (n < 32 ? n : 32) / 2; off >= 1; off >>= 1) {
             const T ov = __shfl_xor_sync(kFull, bv, off);
             const int oe = __shfl_xor_sync(kFull, be, off);
-            if (oe != 0x7fffffff && (be == 0x7fffffff || ov < bv || (ov == bv && oe < be))) {
+            if (ov < bv || (ov == bv && oe < be)) {
                 bv = ov;
                 be = oe;
             }
