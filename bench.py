@@ -73,14 +73,19 @@ def select_config(name):
     return frames
 
 
-def _traffic(config):
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture, or None."""
+def _capture(config):
+    """The dominant kernel's ncu figures for this config (profiles/r1_traffic.json), or {}."""
     try:
         with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as fh:
-            d = json.load(fh)[config]
-        return d["dram_read_bytes"] + d["dram_write_bytes"]
+            return json.load(fh)[config]
     except Exception:
-        return None
+        return {}
+
+
+def _traffic(config):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture, or None."""
+    d = _capture(config)
+    return d["dram_read_bytes"] + d["dram_write_bytes"] if "dram_read_bytes" in d else None
 
 
 def _peaks():
@@ -369,6 +374,15 @@ def run_gpu(args):
                              "bytes_per_frame": bytes_frame + rec_bytes_frame},
             "clocks": clk,
         }
+        cap = _capture(args.config)
+        if "warp_instructions" in cap:
+            # issue view of the same kernel: warp instructions per frame (ncu,
+            # committed capture) x the live frame rate vs 4 issue slots/clk/SM
+            ipf = cap["warp_instructions"] / cap["frames_per_launch"]
+            peak_i = sms * 4 * sm_mhz * 1e6 / 1e9
+            line["roofline_issue"] = {"bound": "issue", "achieved": ipf * kern_fps / 1e9, "peak": peak_i,
+                                      "unit": "G warp-inst/s", "frac": ipf * kern_fps / 1e9 / peak_i,
+                                      "inst_per_frame": ipf}
         if not args.no_cpu and ws == 1:
             line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
         print(json.dumps(line), flush=True)

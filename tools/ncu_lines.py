@@ -12,7 +12,8 @@ h = rows[1]
 iA, iS, iE = h.index("Address"), h.index("Source"), h.index("Instructions Executed")
 iW = h.index("Warp Stall Sampling (All Samples)")
 metric = os.environ.get("NCU_LINES_METRIC", "exec")  # exec | stall | wave | excess
-iX = {"wave": h.index("L1 Wavefronts Shared"), "excess": h.index("L1 Wavefronts Shared Excessive")}.get(metric)
+iX = {"wave": "L1 Wavefronts Shared", "excess": "L1 Wavefronts Shared Excessive"}.get(metric)
+iX = h.index(iX) if iX else None
 execs = []
 for r in rows[2:]:
     if len(r) > iE and r[iA].startswith("0x"):
