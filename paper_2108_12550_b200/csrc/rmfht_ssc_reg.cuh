@@ -124,9 +124,9 @@ __device__ __forceinline__ uint32_t ssc_node(const T (&x)[NodeL<S>::V], int lane
     }
 }
 
-// column-form affine map from a device record (cols, b, icols, A^-1 b)
+// linear part of an affine map from its columns (held in registers)
 template <int MM>
-__device__ __forceinline__ unsigned rec_lin(const uint16_t* cols, unsigned x) {
+__device__ __forceinline__ unsigned rec_lin(const unsigned* cols, unsigned x) {
     unsigned v = 0;
 #pragma unroll
     for (int k = 0; k < MM; k++) v ^= ((x >> k) & 1u) ? (unsigned)cols[k] : 0u;
@@ -155,8 +155,13 @@ __global__ void __launch_bounds__(256) aut_ssc_reg_kernel(rmfht::Params<T> prm) 
             const uint16_t* g = prm.maps + ((size_t)f * P + p) * REC;
             if (lane < REC) recw[lane] = g[lane];
             __syncwarp();
-            const uint16_t* cols = recw;
-            const uint16_t* icols = recw + MM + 1;
+            // the map's columns in registers (every index below is an XOR of them)
+            unsigned cols[MM], icols[MM];
+#pragma unroll
+            for (int k = 0; k < MM; k++) {
+                cols[k] = recw[k];
+                icols[k] = recw[MM + 1 + k];
+            }
             // apply_perm (automorphism.py:164-170): x[j] = alpha[sigma^-1(j)],
             // j = k*32 + lane
             T x[V];
@@ -198,21 +203,25 @@ __global__ void __launch_bounds__(256) aut_ssc_reg_kernel(rmfht::Params<T> prm) 
                 pass_sum = q == 0 ? s : pass_sum + s;
             }
             const T score = pass_sum;
-            // the un-permuted codeword, bit-packed: word k of lane k
-            uint32_t myword = 0;
-            const unsigned sl = rec_lin<MM>(cols, (unsigned)lane) ^ bsh;
+            const bool better = bestp < 0 || score > best;  // first strictly largest (warp-uniform)
+            if (better || prm.att_cw) {
+                // the un-permuted codeword, bit-packed: word k of lane k (only
+                // for a new best, or when every decode's codeword is wanted)
+                uint32_t myword = 0;
+                const unsigned sl = rec_lin<MM>(cols, (unsigned)lane) ^ bsh;
 #pragma unroll
-            for (int k = 0; k < V; k++) {
-                const unsigned s = sl ^ rec_lin<MM>(cols, 32u * k);
-                const uint32_t wv = __ballot_sync(kFull, (cww[s & 31u] >> (s >> 5)) & 1u);
-                if (lane == k) myword = wv;
+                for (int k = 0; k < V; k++) {
+                    const unsigned s = sl ^ rec_lin<MM>(cols, 32u * k);
+                    const uint32_t wv = __ballot_sync(kFull, (cww[s & 31u] >> (s >> 5)) & 1u);
+                    if (lane == k) myword = wv;
+                }
+                if (prm.att_cw && lane < V) prm.att_cw[((size_t)f * P + p) * V + lane] = myword;
+                if (better) bestword = myword;
             }
             if (prm.att_pm && lane == 0) prm.att_pm[(size_t)f * P + p] = score;
-            if (prm.att_cw && lane < V) prm.att_cw[((size_t)f * P + p) * V + lane] = myword;
-            if (bestp < 0 || score > best) {  // first strictly largest
+            if (better) {
                 best = score;
                 bestp = p;
-                bestword = myword;
             }
             __syncwarp();
         }
