@@ -124,9 +124,14 @@ struct alignas(16) WS2 {
     // The LM lane partials of the root permutation extension share the space
     // (they are dead before the first FHT node).
     static constexpr int VMAX = cmax(4, (R == 1 ? C::N : (C::N >> (R - 1))) / C::LPP);
+    // The inner permutation nodes' vectors (vbuf, at the node's start) and
+    // output bits (ubits, at its end) are dead whenever an FHT node runs, so
+    // they share the space too; the largest inner node has N/2 elements.
     union alignas(16) {
         float wsp[32][VMAX];  // 16-byte chunks XOR-swizzled per lane (wsp_idx): conflict-free STS.128
         float lmp[2 * L][32];
+        float vbuf[R >= 3 ? L * C::N / 2 : 1];
+        uint8_t ubits[R >= 3 ? L * C::N / 2 : 1];
     };
     // element k of lane `lane`'s row
     __device__ __forceinline__ static int wsp_idx(int lane, int k) {
@@ -143,8 +148,6 @@ struct alignas(16) WS2 {
     float smag[L * (C::SPCMAX > 16 ? C::SPCMAX : 16)];
     uint8_t ssgn[L * C::SPCMAX];
     uint16_t sord[L * 16];
-    float vbuf[R >= 3 ? L * C::N : 1];  // inner permutation nodes
-    uint8_t ubits[R >= 3 ? L * C::N : 1];
     int next_map;
 };
 
