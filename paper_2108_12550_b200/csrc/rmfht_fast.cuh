@@ -1252,11 +1252,11 @@ constexpr size_t smem_bytes2(int nwarps) {
     return 2048 + size_t(1 << MM) * 4 * size_t(nwarps) + sizeof(WS2<R, MM, L>) * size_t(nwarps);
 }
 
-// warps per CTA: the largest multiple of 4 (at most 24, i.e. an 80-register
+// warps per CTA: the largest multiple of 4 (at most 32, i.e. a 64-register
 // cap) whose LLR copies and scratch fit in 227 KB of shared memory
 template <int R, int MM, int L>
 constexpr int fast_warps() {
-    int w = 24;
+    int w = 32;
     while (w > 4 && smem_bytes2<R, MM, L>(w) > 227 * 1024) w -= 4;
     return w;
 }
