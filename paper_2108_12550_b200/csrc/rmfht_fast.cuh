@@ -134,12 +134,13 @@ struct alignas(16) WS2 {
         uint8_t ubits[R >= 3 ? L * C::N / 2 : 1];
     };
     // element k of lane `lane`'s row
-    __device__ __forceinline__ static int wsp_idx(int lane, int k) {
+    // t: extra per-node chunk twist (FhtLayout::twist) for the transposed FHT reads
+    __device__ __forceinline__ static int wsp_idx(int lane, int k, int t = 0) {
         constexpr int G = VMAX / 4;  // 16-byte chunks per row
         const int swz = G >= 8 ? (lane & 7) : ((lane / (8 / G)) & (G - 1));
-        return (((k >> 2) ^ swz) << 2) | (k & 3);
+        return (((k >> 2) ^ swz ^ t) << 2) | (k & 3);
     }
-    __device__ __forceinline__ float& wspk(int lane, int k) { return wsp[lane][wsp_idx(lane, k)]; }
+    __device__ __forceinline__ float& wspk(int lane, int k, int t = 0) { return wsp[lane][wsp_idx(lane, k, t)]; }
     int sel_src[2 * L], sel_bin[2 * L];
     float sel_w[2 * L], sel_pm[2 * L];
     int8_t l0[MM + 1][L], l1[MM + 1][L], l2[MM + 1][L], rootchain[L], ord[2 * L];
@@ -267,15 +268,54 @@ __device__ unsigned long long g_stats[256];
 #define RMFHT_STAT_ADD(i, v) do { } while (0)
 #endif
 
+// Where an FHT node's transform values live after the butterflies.
+// Default: element (bin) e = k * LPP + u sits in register slot k of lane u.
+// TR ("transposed lane stages", 8 lanes per path, V >= 8): the register
+// stages run in the default layout, the vector is then transposed through
+// the spill rows so that the last three stages (the lane bits of e) are
+// register stages too — no shuffles.  Afterwards lane u holds, in slot
+// k = g * 8 + j, element e = (u * G + g) * 8 + j (G = V / 8).
+template <int R, int MM, int L, int SS>
+struct FhtLayout {
+    using C = Cfg<R, MM, L>;
+    using LV = Lv<SS, C::LPP>;
+    static constexpr int V = LV::V;
+    static constexpr bool TSHAPE = C::LPP == 8 && WS2<R, MM, L>::VMAX == 32;
+    static constexpr bool TR = TSHAPE && LV::full && V >= 8;
+    static constexpr int G = TR ? V / 8 : 1;
+    __device__ __forceinline__ static int bin(int k, int u) {
+        if constexpr (TR) return ((u * G + (k >> 3)) << 3) | (k & 7);
+        else return LV::full ? k * C::LPP + u : u;
+    }
+    __device__ __forceinline__ static int owner(int b) {  // lane of the group holding bin b
+        if constexpr (TR) return (b >> 3) / G;
+        else return LV::full ? b % C::LPP : b;
+    }
+    __device__ __forceinline__ static int slot(int b) {
+        if constexpr (TR) return (((b >> 3) % G) << 3) | (b & 7);
+        else return LV::full ? b / C::LPP : 0;
+    }
+    // chunk twist of the spill rows (XOR-ed into the lane swizzle) so that the
+    // transposed reads are conflict-free: LDS.128 (V = 32) phases are one
+    // path, LDS.64 (V = 16) phases two paths, LDS.32 (V = 8) all four
+    __device__ __forceinline__ static int twist(int p) {
+        if constexpr (TSHAPE && V == 16) return 4 * (p & 1);
+        else if constexpr (TSHAPE && V == 8) return 2 * p;
+        else return 0;
+    }
+};
+
 // Rare path of fht_node (more candidates than kCap): exact K-round selection
 // per path, then the pool — as the reference-order kernel does it.
 template <int R, int MM, int L, int SS>
 __device__ __noinline__ void fht_fallback(WS2<R, MM, L>* wsp_, int lane, float llrabs) {
     using C = Cfg<R, MM, L>;
     using LV = Lv<SS, C::LPP>;
+    using FL = FhtLayout<R, MM, L, SS>;
     constexpr int n = LV::n, V = LV::V, K = cmin(L, n);
     auto& ws = *wsp_;
     const int p = lane / C::LPP, u = lane % C::LPP;
+    const int tw = FL::twist(p);
     const bool act = LV::full || u < n;
         // rare: exact K-round selection per path, then the pool (as rmfht_kernels.cuh)
         {
@@ -289,8 +329,8 @@ __device__ __noinline__ void fht_fallback(WS2<R, MM, L>* wsp_, int lane, float l
             int bb = 0x7fffffff;
 #pragma unroll
             for (int k = 0; k < V; k++) {
-                const int e = LV::full ? k * C::LPP + u : u;
-                const float wk = ws.wspk(lane, k);
+                const int e = FL::bin(k, u);
+                const float wk = ws.wspk(lane, k, tw);
                 const float a = fabsf(wk);
                 if (act && !((taken >> k) & 1ull) && (a > bv || (a == bv && e < bb))) { bv = a; bb = e; bw = wk; }
             }
@@ -300,7 +340,7 @@ __device__ __noinline__ void fht_fallback(WS2<R, MM, L>* wsp_, int lane, float l
                 const int ob = __shfl_xor_sync(kFull, bb, off);
                 if (ov > bv || (ov == bv && ob < bb)) { bv = ov; bb = ob; bw = ow; }
             }
-            if (act && (LV::full ? (bb % C::LPP) == u : bb == u)) taken |= 1ull << (LV::full ? bb / C::LPP : 0);
+            if (act && FL::owner(bb) == u) taken |= 1ull << FL::slot(bb);
             if (u == 0) {
                 ws.ca[p * K + rr] = bv;
                 ws.cb[p * K + rr] = bb;
@@ -352,13 +392,13 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
     for (int k = 1; k < V; k++) part += fabsf(x[k]);
     const float llrabs = group_sum_tree<C::LPP, LV::act>(part);
     // butterflies (:28-48): register bits (high) first, then lane bits
+    using FL = FhtLayout<R, MM, L, SS>;
+    const int tw = FL::twist(p);
     float w[V];
 #pragma unroll
     for (int k = 0; k < V; k++) w[k] = act ? x[k] : 0.f;
-    constexpr int LOGV = clog2(V);
-#pragma unroll
-    for (int st = 0; st < LOGV; st++) {
-        const int hr = V >> (st + 1);
+    // stages on register-slot bit hr (lo = slot k, hi = slot k + hr)
+    auto reg_stage = [&](const int hr) {
         if (hr >= 2) {
             // two butterflies per instruction: (k, k+1) against (k+hr, k+hr+1)
 #pragma unroll
@@ -379,7 +419,39 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
                 w[k + 1] = hi + lo;
             }
         }
-    }
+    };
+    constexpr int LOGV = clog2(V);
+#pragma unroll
+    for (int st = 0; st < LOGV; st++) reg_stage(V >> (st + 1));
+    if constexpr (FL::TR) {
+        // transpose through the spill rows: lane u of path p gathers, for
+        // every j < 8, slots u*G .. u*G+G-1 of row p*8 + j (element
+        // (u*G + g)*8 + j) into slot g*8 + j; then the lane-bit stages
+        // (half = 4, 2, 1 on e) are register stages on slot bits 2..0
+        constexpr int G = FL::G;
+#pragma unroll
+        for (int k = 0; k < V; k += 4)
+            *reinterpret_cast<float4*>(&ws.wspk(lane, k, tw)) = make_float4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const int row = p * 8 + j;
+            const float* src = &ws.wspk(row, u * G, tw);
+            if constexpr (G == 4) {
+                const float4 v = *reinterpret_cast<const float4*>(src);
+                w[j] = v.x; w[8 + j] = v.y; w[16 + j] = v.z; w[24 + j] = v.w;
+            } else if constexpr (G == 2) {
+                const float2 v = *reinterpret_cast<const float2*>(src);
+                w[j] = v.x; w[8 + j] = v.y;
+            } else {
+                w[j] = *src;
+            }
+        }
+        __syncwarp();  // every row read before the transform is spilled again
+        reg_stage(4);
+        reg_stage(2);
+        reg_stage(1);
+    } else {
     constexpr int LOGA = clog2(LV::act);
 #pragma unroll
     for (int st = 0; st < LOGA; st++) {
@@ -399,6 +471,7 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
             const float o = __shfl_xor_sync(kFull, w[0], half);
             w[0] = __fmaf_rn(sg, w[0], o);
         }
+    }
     }
     // path maximum and the pool threshold tau = L-th smallest path-best pm
     // (a warp-wide maximum: one REDUX on order-preserving integer keys; cbest
@@ -442,10 +515,10 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
     if constexpr (V >= 4) {
 #pragma unroll
         for (int k = 0; k < V; k += 4)
-            *reinterpret_cast<float4*>(&ws.wspk(lane, k)) = make_float4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+            *reinterpret_cast<float4*>(&ws.wspk(lane, k, tw)) = make_float4(w[k], w[k + 1], w[k + 2], w[k + 3]);
     } else {
 #pragma unroll
-        for (int k = 0; k < V; k++) ws.wspk(lane, k) = w[k];
+        for (int k = 0; k < V; k++) ws.wspk(lane, k, tw) = w[k];
     }
     __syncwarp();
     RMFHT_STAT(SS * 8 + 0);
@@ -461,8 +534,8 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
         float myw = 0.f;
         if (cnt > 0) {
             const int k = (sizeof(MaskT) == 8 ? __ffsll((long long)mask) : __ffs((int)mask)) - 1;
-            mybin = LV::full ? k * C::LPP + u : u;
-            myw = ws.wspk(lane, k);
+            mybin = FL::bin(k, u);
+            myw = ws.wspk(lane, k, tw);
         }
         const int bin = __shfl_sync(kFull, mybin, p * C::LPP + owner);
         const float wv = __shfl_sync(kFull, myw, p * C::LPP + owner);
@@ -480,6 +553,56 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
         }
         __syncwarp();
     } else {
+    // General case: L rounds of warp-wide minimum selection over the pool key
+    // (pm, source path, bin) (:120), each lane offering its best remaining
+    // candidate.  The per-path top-K cut (:116, K = L here) can only exclude
+    // a pool top-L candidate X when a candidate Z of the same path has the
+    // same pm but a larger |w| and a larger bin (a pm rounding collision);
+    // every pick therefore checks that no other remaining candidate of its
+    // path has its exact pm, and a collision hands the node to the exact
+    // list path below.
+    bool exact_needed = true;
+    if constexpr (K == L) {
+        const u32 pkey = (u32)p << 16;
+        auto lane_best = [&](MaskT m, u32& hi, u32& lo) {
+            hi = 0xffffffffu;
+            lo = 0xffffffffu;
+            while (m) {
+                const int k = (sizeof(MaskT) == 8 ? __ffsll((long long)m) : __ffs((int)m)) - 1;
+                m &= m - 1;
+                const float pmc = pmp + 0.5f * (llrabs - fabsf(ws.wspk(lane, k, tw)));  // :119
+                const u32 h = float_key(pmc), l = pkey | (u32)FL::bin(k, u);
+                if (h < hi || (h == hi && l < lo)) { hi = h; lo = l; }
+            }
+        };
+        MaskT rem = mask;
+        u32 hi, lo;
+        lane_best(rem, hi, lo);
+        bool coll = false;
+#pragma unroll 1
+        for (int r = 0; r < L; r++) {
+            const u32 hmin = __reduce_min_sync(kFull, hi);
+            const u32 lmin = __reduce_min_sync(kFull, hi == hmin ? lo : 0xffffffffu);
+            const int dup = __reduce_add_sync(kFull, (hi == hmin && (lo >> 16) == (lmin >> 16)) ? 1 : 0);
+            coll |= dup > 1;
+            if (hi == hmin && lo == lmin) {
+                const int bin = (int)(lo & 0xffffu);
+                const int k = FL::slot(bin);
+                ws.sel_src[r] = p;
+                ws.sel_bin[r] = bin;
+                ws.sel_w[r] = ws.wspk(lane, k, tw);
+                ws.sel_pm[r] = key_float(hmin);
+                rem &= ~((MaskT)1 << k);
+                lane_best(rem, hi, lo);
+                coll |= hi == hmin;  // same path, same pm, still in the pool
+            }
+        }
+        exact_needed = __any_sync(kFull, coll);
+        __syncwarp();
+        RMFHT_STAT(SS * 8 + 6);
+        if (exact_needed) RMFHT_STAT(SS * 8 + 7);
+    }
+    if (exact_needed) {
     // candidates per path (for the per-path top-K rule, fht_decode.py:116) and
     // each lane's position in the warp list (inclusive prefix sum)
     int pcnt = cnt;
@@ -506,9 +629,9 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
         while (mk) {
             const int k = sizeof(MaskT) == 8 ? __ffsll((long long)mk) - 1 : __ffs((int)mk) - 1;
             mk &= mk - 1;
-            const float v = ws.wspk(lane, k);
+            const float v = ws.wspk(lane, k, tw);
             const float a = fabsf(v);
-            const int bin = LV::full ? k * C::LPP + u : u;
+            const int bin = FL::bin(k, u);
             const float pmc = pmp + 0.5f * (llrabs - a);  // :119
             u32 kb = __float_as_uint(pmc);
             kb ^= (kb >> 31) ? 0xffffffffu : 0x80000000u;  // order-preserving for any sign
@@ -576,6 +699,7 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
     } else {
         RMFHT_STAT(SS * 8 + 3);
         fht_fallback<R, MM, L, SS>(&cx.ws, lane, llrabs);
+    }
     }
     }
     // survivors: pm, lineage; my group's codeword bits
@@ -1302,7 +1426,9 @@ __global__ void __launch_bounds__(32 * fast_warps<R, MM, L>(), 1) decode_kernel2
     auto prefetch_alpha = [&](long long it) {
         if (it >= items) return;
         __syncwarp();  // every lane is past its last read of the current LLRs
-        const char* ga = reinterpret_cast<const char*>(prm.llr + (it / prm.M) * N);
+        // frame of the item (32-bit division whenever the item count allows)
+        const long long f = items <= 0xffffffffLL ? (long long)((u32)it / (u32)prm.M) : it / prm.M;
+        const char* ga = reinterpret_cast<const char*>(prm.llr + f * N);
         for (int i = lane; i < N / 4; i += 32) cp_async16(asa + 16u * i, ga + 16 * i);
         cp_async_commit();
     };
