@@ -274,7 +274,9 @@ __device__ unsigned long long g_stats[256];
 // stages run in the default layout, the vector is then transposed through
 // the spill rows so that the last three stages (the lane bits of e) are
 // register stages too — no shuffles.  Afterwards lane u holds, in slot
-// k = g * 8 + j, element e = (u * G + g) * 8 + j (G = V / 8).
+// k = j * G + g, element e = (u * G + g) * 8 + j (G = V / 8), so each
+// transposed LDS.128 / LDS.64 fills consecutive slots (register pairs for
+// the packed butterflies).
 template <int R, int MM, int L, int SS>
 struct FhtLayout {
     using C = Cfg<R, MM, L>;
@@ -284,7 +286,7 @@ struct FhtLayout {
     static constexpr bool TR = TSHAPE && LV::full && V >= 8;
     static constexpr int G = TR ? V / 8 : 1;
     __device__ __forceinline__ static int bin(int k, int u) {
-        if constexpr (TR) return ((u * G + (k >> 3)) << 3) | (k & 7);
+        if constexpr (TR) return ((u * G + k % G) << 3) | (k / G);
         else return LV::full ? k * C::LPP + u : u;
     }
     __device__ __forceinline__ static int owner(int b) {  // lane of the group holding bin b
@@ -292,7 +294,7 @@ struct FhtLayout {
         else return LV::full ? b % C::LPP : b;
     }
     __device__ __forceinline__ static int slot(int b) {
-        if constexpr (TR) return (((b >> 3) % G) << 3) | (b & 7);
+        if constexpr (TR) return (b & 7) * G + (b >> 3) % G;
         else return LV::full ? b / C::LPP : 0;
     }
     // chunk twist of the spill rows (XOR-ed into the lane swizzle) so that the
@@ -426,8 +428,8 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
     if constexpr (FL::TR) {
         // transpose through the spill rows: lane u of path p gathers, for
         // every j < 8, slots u*G .. u*G+G-1 of row p*8 + j (element
-        // (u*G + g)*8 + j) into slot g*8 + j; then the lane-bit stages
-        // (half = 4, 2, 1 on e) are register stages on slot bits 2..0
+        // (u*G + g)*8 + j) into slot j*G + g; then the lane-bit stages
+        // (half = 4, 2, 1 on e) are register stages on slot bits 4G, 2G, G
         constexpr int G = FL::G;
 #pragma unroll
         for (int k = 0; k < V; k += 4)
@@ -439,18 +441,18 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
             const float* src = &ws.wspk(row, u * G, tw);
             if constexpr (G == 4) {
                 const float4 v = *reinterpret_cast<const float4*>(src);
-                w[j] = v.x; w[8 + j] = v.y; w[16 + j] = v.z; w[24 + j] = v.w;
+                w[4 * j] = v.x; w[4 * j + 1] = v.y; w[4 * j + 2] = v.z; w[4 * j + 3] = v.w;
             } else if constexpr (G == 2) {
                 const float2 v = *reinterpret_cast<const float2*>(src);
-                w[j] = v.x; w[8 + j] = v.y;
+                w[2 * j] = v.x; w[2 * j + 1] = v.y;
             } else {
                 w[j] = *src;
             }
         }
         __syncwarp();  // every row read before the transform is spilled again
-        reg_stage(4);
-        reg_stage(2);
-        reg_stage(1);
+        reg_stage(4 * G);
+        reg_stage(2 * G);
+        reg_stage(G);
     } else {
     constexpr int LOGA = clog2(LV::act);
 #pragma unroll
@@ -795,6 +797,10 @@ __device__ __forceinline__ u64 spc_node_v1(Ctx2<R, MM, L>& cx, float xv, int8_t*
             const float cc = __shfl_sync(kFull, cand, c);
             r2 += (cc < cand) || (cc == cand && c < lane);
         }
+        // no flip survives and the keeps are already in slot order: the state
+        // is unchanged, and since the later positions are at least as
+        // unreliable (a_{j+1} >= a_j), every later split keeps it too
+        if (__all_sync(kFull, lane >= 2 * L || ((lane & 1) ? r2 >= L : r2 == (lane >> 1)))) break;
         if (lane < 2 * L && r2 < L) {
             const int flip = lane & 1;
             ws.cpm[r2] = cand;
@@ -1371,7 +1377,7 @@ struct AttHdr {
 };
 
 template <int R, int MM, int L>
-constexpr size_t smem_bytes2(int nwarps) {
+__host__ __device__ constexpr size_t smem_bytes2(int nwarps) {
     // 2 KB alignment pad + per-warp LLR copy (N floats, N-aligned) + per-warp scratch
     return 2048 + size_t(1 << MM) * 4 * size_t(nwarps) + sizeof(WS2<R, MM, L>) * size_t(nwarps);
 }
@@ -1379,7 +1385,7 @@ constexpr size_t smem_bytes2(int nwarps) {
 // warps per CTA: the largest multiple of 4 (at most 32, i.e. a 64-register
 // cap) whose LLR copies and scratch fit in 227 KB of shared memory
 template <int R, int MM, int L>
-constexpr int fast_warps() {
+__host__ __device__ constexpr int fast_warps() {
     int w = 32;
     while (w > 4 && smem_bytes2<R, MM, L>(w) > 227 * 1024) w -= 4;
     return w;
@@ -1398,7 +1404,10 @@ __global__ void __launch_bounds__(32 * fast_warps<R, MM, L>(), 1) decode_kernel2
     constexpr int N = C::N, S = C::S, REC = 2 * MM + 2, V = LV::V;
     static_assert(N >= 32 && L <= 8 && N <= 512, "fast kernel: 32 <= N <= 512, L <= 8");
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = lane_id();
+    // the launch always uses fast_warps() warps (prepare_fast): a compile-time
+    // count keeps the per-warp scratch addresses cheap to rematerialise
+    constexpr int nwarps = fast_warps<R, MM, L>();
+    const int warp = threadIdx.x >> 5, lane = lane_id();
     // per-warp frame LLRs, each 2 KB aligned in the shared window, then the scratch
     const u32 raw_saddr = (u32)__cvta_generic_to_shared(smem_raw);
     const u32 pad = ((raw_saddr + 2047u) & ~2047u) - raw_saddr;
