@@ -138,7 +138,7 @@ struct alignas(16) WS2 {
     __device__ __forceinline__ static int wsp_idx(int lane, int k, int t = 0) {
         constexpr int G = VMAX / 4;  // 16-byte chunks per row
         const int swz = G >= 8 ? (lane & 7) : ((lane / (8 / G)) & (G - 1));
-        return (((k >> 2) ^ swz ^ t) << 2) | (k & 3);
+        return k ^ ((swz ^ t) << 2);  // chunk (k >> 2) ^ swz ^ t, word k & 3
     }
     __device__ __forceinline__ float& wspk(int lane, int k, int t = 0) { return wsp[lane][wsp_idx(lane, k, t)]; }
     int sel_src[2 * L], sel_bin[2 * L];
@@ -580,14 +580,23 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
         MaskT rem = mask;
         u32 hi, lo;
         lane_best(rem, hi, lo);
-        bool coll = false;
+        // picks come in ascending pm order, so a same-path pm collision that
+        // matters (a remaining candidate with the pm of a pick) can only be at
+        // the last pick's pm: track the paths picked at that pm
+        u32 hlast = 0xffffffffu, lastpaths = 0u;
 #pragma unroll 1
         for (int r = 0; r < L; r++) {
             const u32 hmin = __reduce_min_sync(kFull, hi);
-            const u32 lmin = __reduce_min_sync(kFull, hi == hmin ? lo : 0xffffffffu);
-            const int dup = __reduce_add_sync(kFull, (hi == hmin && (lo >> 16) == (lmin >> 16)) ? 1 : 0);
-            coll |= dup > 1;
-            if (hi == hmin && lo == lmin) {
+            const u32 eq = __ballot_sync(kFull, hi == hmin);
+            int wl = __ffs(eq) - 1;
+            if (eq & (eq - 1)) {  // several lanes at this pm: the lowest (path, bin)
+                const u32 lmin = __reduce_min_sync(kFull, hi == hmin ? lo : 0xffffffffu);
+                wl = __ffs(__ballot_sync(kFull, hi == hmin && lo == lmin)) - 1;
+            }
+            const u32 pbit = 1u << (wl / C::LPP);
+            lastpaths = hmin == hlast ? (lastpaths | pbit) : pbit;
+            hlast = hmin;
+            if (lane == wl) {
                 const int bin = (int)(lo & 0xffffu);
                 const int k = FL::slot(bin);
                 ws.sel_src[r] = p;
@@ -596,10 +605,9 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
                 ws.sel_pm[r] = key_float(hmin);
                 rem &= ~((MaskT)1 << k);
                 lane_best(rem, hi, lo);
-                coll |= hi == hmin;  // same path, same pm, still in the pool
             }
         }
-        exact_needed = __any_sync(kFull, coll);
+        exact_needed = __any_sync(kFull, hi == hlast && ((lastpaths >> p) & 1u));
         __syncwarp();
         RMFHT_STAT(SS * 8 + 6);
         if (exact_needed) RMFHT_STAT(SS * 8 + 7);

@@ -51,10 +51,11 @@ assert fn(st.ctypes.data_as(ctypes.c_void_p)) == 0
 items = B * 20
 print(f"items {items}")
 for ss in range(3, 9):
-    n, common, gen, fb, tot, over = (int(st[ss * 8 + k]) for k in (0, 1, 2, 3, 4, 5))
+    n, common, gen, fb, tot, over, greedy, exact = (int(st[ss * 8 + k]) for k in range(8))
     if n:
-        print(f"FHT 2^{ss}: {n / items:.2f}/item  common {common / n:.3f}  general {gen / n:.3f} "
-              f"(over {over / n:.3f})  fallback {fb / n:.4f}  mean cand {tot / n:.1f}")
+        print(f"FHT 2^{ss}: {n / items:.2f}/item  common {common / n:.3f}  greedy {greedy / n:.3f} "
+              f"(collision -> exact list {exact / n:.3f}; over {over / n:.3f})  fallback {fb / n:.4f}  "
+              f"mean cand {tot / n:.1f}")
 cnt, s1, s2, mx = int(st[202]), int(st[200]), int(st[201]) * 1024, int(st[203])
 if cnt:
     mean = s1 / cnt
