@@ -1437,7 +1437,12 @@ __global__ void __launch_bounds__(32 * fast_warps<R, MM, L>(), 1) decode_kernel2
         if (it >= items || !PM) return;
         const u32 rsa = (u32)__cvta_generic_to_shared(ws.recs[buf]);
         const char* gr = reinterpret_cast<const char*>(prm.maps + (size_t)it * S * REC);
-        for (int i = lane; i < WS::RECW / 2; i += 32) cp_async4(rsa + 4u * i, gr + 4 * i);
+        constexpr int RB = S * REC * 2;  // record bytes per item
+        if (RB % 16 == 0 && (reinterpret_cast<uintptr_t>(prm.maps) & 15u) == 0) {
+            for (int i = lane; i < RB / 16; i += 32) cp_async16(rsa + 16u * i, gr + 16 * i);
+        } else {
+            for (int i = lane; i < WS::RECW / 2; i += 32) cp_async4(rsa + 4u * i, gr + 4 * i);
+        }
         cp_async_commit();
     };
     auto prefetch_alpha = [&](long long it) {
