@@ -1,5 +1,7 @@
 // Kernel-binding unit: instantiates decode_kernel<T, r, m, L> for one dtype
 // and one chunk of RMFHT_CONFIGS; built once per (RMFHT_T, RMFHT_CHUNK).
+#include <cstdlib>
+
 #include "rmfht_fast.cuh"
 #include "rmfht_kernels.cuh"
 #include "rmfht_plan.h"
@@ -89,8 +91,11 @@ int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
     auto* mp = const_cast<rmfht_plan*>(p);
     std::call_once(mp->once, [mp] { mp->prepared_rc = mp->prepare(mp); });
     if (p->prepared_rc != 0) return p->prepared_rc;
-    const size_t items = (size_t)B * p->M;
-    const size_t need = items * rmfht2::work_bytes2<R, MM, L>();
+    // the kernel indexes work items with 32-bit integers: at most 2^30 items
+    // (frames x attempts) per launch, larger batches go in frame chunks
+    const long long chunk = p->max_items / p->M > 0 ? p->max_items / p->M : 1;
+    const long long B0 = B < chunk ? B : chunk;
+    const size_t need = (size_t)B0 * p->M * rmfht2::work_bytes2<R, MM, L>();
     {
         std::lock_guard<std::mutex> g(mp->work_mu);
         if (need > mp->work_cap) {
@@ -101,16 +106,31 @@ int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
             mp->work_cap = need;
         }
     }
-    auto* hdr = static_cast<rmfht2::AttHdr*>(mp->work);
-    auto* bits = reinterpret_cast<unsigned long long*>(static_cast<char*>(mp->work) + items * sizeof(rmfht2::AttHdr));
-    const long long blocks_needed = ((long long)items + p->nwarps - 1) / p->nwarps;
-    const long long grid = blocks_needed < p->grid ? blocks_needed : p->grid;
-    if (p->perms) {
-        rmfht2::decode_kernel2<R, MM, L, true><<<(unsigned)grid, p->nwarps * 32, p->smem, st>>>(prm, hdr, bits);
-    } else if constexpr (L == 1) {
-        rmfht2::decode_kernel2<R, MM, L, false><<<(unsigned)grid, p->nwarps * 32, p->smem, st>>>(prm, hdr, bits);
+    constexpr int N = 1 << MM, NW = N / 32, S = rmfht::maps_per_attempt(R, MM, L), REC = 2 * MM + 2;
+    for (long long f0 = 0; f0 < B; f0 += chunk) {
+        const long long Bc = B - f0 < chunk ? B - f0 : chunk;
+        rmfht::Params<float> q = prm;
+        q.B = Bc;
+        q.llr = prm.llr + f0 * N;
+        if (prm.maps) q.maps = prm.maps + (size_t)f0 * p->M * S * REC;
+        q.cw = prm.cw + f0 * NW;
+        q.pm = prm.pm + f0;
+        q.attempt = prm.attempt + f0;
+        q.path = prm.path + f0;
+        if (prm.att_pm) q.att_pm = prm.att_pm + f0 * p->M;
+        if (prm.att_cw) q.att_cw = prm.att_cw + (size_t)f0 * p->M * NW;
+        const size_t items = (size_t)Bc * p->M;
+        auto* hdr = static_cast<rmfht2::AttHdr*>(mp->work);
+        auto* bits = reinterpret_cast<unsigned long long*>(static_cast<char*>(mp->work) + items * sizeof(rmfht2::AttHdr));
+        const long long blocks_needed = ((long long)items + p->nwarps - 1) / p->nwarps;
+        const long long grid = blocks_needed < p->grid ? blocks_needed : p->grid;
+        if (p->perms) {
+            rmfht2::decode_kernel2<R, MM, L, true><<<(unsigned)grid, p->nwarps * 32, p->smem, st>>>(q, hdr, bits);
+        } else if constexpr (L == 1) {
+            rmfht2::decode_kernel2<R, MM, L, false><<<(unsigned)grid, p->nwarps * 32, p->smem, st>>>(q, hdr, bits);
+        }
+        rmfht2::reduce_kernel2<R, MM, L><<<(unsigned)((Bc + 7) / 8), 256, 0, st>>>(q, hdr, bits);
     }
-    rmfht2::reduce_kernel2<R, MM, L><<<(unsigned)((B + 7) / 8), 256, 0, st>>>(prm, hdr, bits);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(RMFHT_ECUDA, std::string("decode launch: ") + cudaGetErrorString(e));
     return 0;
@@ -135,6 +155,10 @@ int prepare_fast(rmfht_plan* p) {
     p->nwarps = nw;
     p->smem = smem;
     p->grid = sms * per_sm;
+    if (const char* env = std::getenv("RMFHT_MAX_ITEMS")) {
+        const long long v = std::atoll(env);
+        if (v > 0 && v < p->max_items) p->max_items = v;
+    }
     return 0;
 }
 

@@ -768,10 +768,7 @@ __device__ __forceinline__ u64 spc_node_v1(Ctx2<R, MM, L>& cx, float xv, int8_t*
         const float mw = __shfl_sync(kFull, mag, p * C::LPP + w);
         rank += (mw < mag) || (mw == mag && w < u);
     }
-    if (act && rank <= TAU) {
-        ws.smag[p * 16 + rank] = mag;
-        ws.sord[p * 16 + rank] = (uint16_t)u;
-    }
+    if (act && rank <= TAU) ws.smag[p * 16 + rank] = mag;
     __syncwarp();
     // slot state (lane i < L holds slot i): metric, running parity, parent path, flips
     float spm = 0.f, spar = 0.f;
@@ -830,11 +827,12 @@ __device__ __forceinline__ u64 spc_node_v1(Ctx2<R, MM, L>& cx, float xv, int8_t*
     const int fl = __shfl_sync(kFull, sfl, p);
     const u32 psg = (sbal >> (parent * C::LPP)) & AM;
     int b = (int)((psg >> u) & 1u);
-#pragma unroll
-    for (int j = 1; j <= TAU; j++)
-        if ((fl >> j) & 1) b ^= ws.sord[parent * 16 + j] == u;
+    // split j flipped the parent's element of rank j (fl bit j): look up this
+    // element's rank in the parent path
+    const int pr = __shfl_sync(kFull, rank, parent * C::LPP + u);
+    b ^= (fl >> pr) & 1;
     const int tot = (__popc(psg) + __popc(fl)) & 1;
-    if (ws.sord[parent * 16] == u) b ^= tot;
+    if (pr == 0) b ^= tot;
     if (lane < L) {
         ws.pm[lane] = spm;
         lin[lane] = (int8_t)sparent;
@@ -1427,13 +1425,14 @@ __global__ void __launch_bounds__(32 * fast_warps<R, MM, L>(), 1) decode_kernel2
     Ctx2<R, MM, L> cx{ws, alpha_w, nullptr, PM ? 1 : 0, {}, lane, lane / C::LPP, lane % C::LPP, asa};
     static_assert(sizeof(MapR<MM>) == 2 * (2 * MM + 2), "record layout");
     constexpr bool ROOT_INTERNAL = !(R == 1 || R == MM - 1);
-    const long long items = prm.B * (long long)prm.M;
-    const long long stride = (long long)gridDim.x * nwarps;
+    // items < 2^31 per launch (launch_fast splits larger batches)
+    const int items = (int)prm.B * prm.M;
+    const int stride = (int)gridDim.x * nwarps;
     // Prefetch (LDGSTS) of the warp's next work item: its map records into the
     // idle half of ws.recs at item start, its LLRs into the single LLR buffer
     // as soon as the current item has read the frame LLRs for the last time
     // (after the root's g, i.e. before the right half of the tree).
-    auto prefetch_recs = [&](long long it, int buf) {
+    auto prefetch_recs = [&](int it, int buf) {
         if (it >= items || !PM) return;
         const u32 rsa = (u32)__cvta_generic_to_shared(ws.recs[buf]);
         const char* gr = reinterpret_cast<const char*>(prm.maps + (size_t)it * S * REC);
@@ -1445,20 +1444,18 @@ __global__ void __launch_bounds__(32 * fast_warps<R, MM, L>(), 1) decode_kernel2
         }
         cp_async_commit();
     };
-    auto prefetch_alpha = [&](long long it) {
+    auto prefetch_alpha = [&](int it) {
         if (it >= items) return;
         __syncwarp();  // every lane is past its last read of the current LLRs
-        // frame of the item (32-bit division whenever the item count allows)
-        const long long f = items <= 0xffffffffLL ? (long long)((u32)it / (u32)prm.M) : it / prm.M;
-        const char* ga = reinterpret_cast<const char*>(prm.llr + f * N);
+        const char* ga = reinterpret_cast<const char*>(prm.llr + (size_t)((u32)it / (u32)prm.M) * N);
         for (int i = lane; i < N / 4; i += 32) cp_async16(asa + 16u * i, ga + 16 * i);
         cp_async_commit();
     };
     int cur = 0;
-    prefetch_recs((long long)blockIdx.x * nwarps + warp, 0);
-    prefetch_alpha((long long)blockIdx.x * nwarps + warp);
-    for (long long base = (long long)blockIdx.x * nwarps; base < items; base += stride) {
-        const long long item = base + warp;
+    prefetch_recs((int)blockIdx.x * nwarps + warp, 0);
+    prefetch_alpha((int)blockIdx.x * nwarps + warp);
+    for (int base = (int)blockIdx.x * nwarps; base < items; base += stride) {
+        const int item = base + warp;
         if (item < items) {
 #ifdef RMFHT_STATS
             const long long t_item = clock64();

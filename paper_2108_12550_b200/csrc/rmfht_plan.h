@@ -22,6 +22,7 @@ struct rmfht_plan {
     int force_generic = 0;
     int aut = 0;  // Aut-SSC plan (RMFHT_AUT_SSC): M = P single-map SSC decodes per frame
     int S, nwarps, grid;
+    long long max_items = 1LL << 30;  // throughput kernel: work items per launch (env RMFHT_MAX_ITEMS, tests)
     size_t smem;
     std::vector<int> sizes;
     LaunchFn launch;

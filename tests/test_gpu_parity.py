@@ -187,3 +187,23 @@ def test_stream_decoder_matches_direct_launch():
         assert np.array_equal(got[i]["cw"].numpy().view(np.uint32), ref["cw_packed"])
         assert np.array_equal(got[i]["pm"].numpy(), ref["pm"])
         assert np.array_equal(got[i]["attempt"].numpy(), ref["attempt"])
+
+
+def test_chunked_launch_matches_single_launch(monkeypatch):
+    """Batches above the per-launch item limit go in frame chunks
+    (launch_fast); a tiny limit (RMFHT_MAX_ITEMS, read when the plan binds)
+    must reproduce the single-launch result on every field, diag included."""
+    from paper_2108_12550_b200.channel_model import synthetic_frames
+    from paper_2108_12550_b200.decoder import Plan
+    from paper_2108_12550_b200.rm_core import build_code
+    spec = build_code(2, 9)
+    _, llr = synthetic_frames(spec, 2.5, 77, seed=21)
+    one = Plan(2, 9, 4, 20, True, "f32")
+    _, rec = one.sample(77, seed=4)
+    a = one.decode(llr, records=rec, diag=True)
+    monkeypatch.setenv("RMFHT_MAX_ITEMS", "200")  # 10 frames (200 items) per launch: 8 chunks
+    many = Plan(2, 9, 4, 20, True, "f32")
+    b = many.decode(llr, records=rec, diag=True)
+    for k in ("cw", "pm", "attempt", "path", "att_pm", "att_cw"):
+        if k in a:
+            assert np.array_equal(a[k], b[k]), k
