@@ -92,18 +92,12 @@ __global__ void __launch_bounds__(256) sample_kernel(SampleArgs a, uint16_t* rec
     const long long items = a.B * (long long)a.M;
     const long long groups = (items + 31) / 32;
     const int lane = threadIdx.x & 31;
-    const long long nwarps = (long long)gridDim.x * blockDim.x / 32;
-    for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; w < groups * a.S; w += nwarps) {
-        const int s = (int)(w % a.S);
-        const long long item = (w / a.S) * 32 + lane;
-        if (item >= items) continue;
-        const long long f = a.frame0 + item / a.M;
-        const int at = (int)(item % a.M);
+    auto one = [&](int s, long long item, long long f, int at) {
         uint16_t* o = rec + ((size_t)item * a.S + s) * (2 * MG + 2);
         const int mn = a.sizes[s];
         if (a.identity_root && at == 0 && s < a.L) {
             rmfht_maps::write_identity(mn, MG, nullptr, o);
-            continue;
+            return;
         }
         const uint64_t key = rmfht_maps::slot_key(a.seed, f, at, s);
         uint32_t* o32 = reinterpret_cast<uint32_t*>(o);
@@ -111,6 +105,26 @@ __global__ void __launch_bounds__(256) sample_kernel(SampleArgs a, uint16_t* rec
         else if (mn == MG - 1 && MG > 1) draw_store<(MG > 1 ? MG - 1 : 1), MG>(key, o32);
         else if (mn == MG - 2 && MG > 2) draw_store<(MG > 2 ? MG - 2 : 1), MG>(key, o32);
         else draw_store_rt<MG>(key, mn, o);
+    };
+    if (groups * a.S < (1LL << 31)) {
+        // 32-bit index arithmetic (the 64-bit divisions cost as much as a map's RNG)
+        const unsigned total = (unsigned)(groups * a.S), S = (unsigned)a.S, M = (unsigned)a.M;
+        const unsigned nw = gridDim.x * blockDim.x / 32;
+        for (unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) / 32; w < total; w += nw) {
+            const unsigned g = w / S, s = w - g * S;
+            const unsigned item = g * 32 + lane;
+            if (item >= (unsigned)items) continue;
+            const unsigned fr = item / M;
+            one((int)s, (long long)item, a.frame0 + fr, (int)(item - fr * M));
+        }
+        return;
+    }
+    const long long nwarps = (long long)gridDim.x * blockDim.x / 32;
+    for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; w < groups * a.S; w += nwarps) {
+        const int s = (int)(w % a.S);
+        const long long item = (w / a.S) * 32 + lane;
+        if (item >= items) continue;
+        one(s, item, a.frame0 + item / a.M, (int)(item % a.M));
     }
 }
 
