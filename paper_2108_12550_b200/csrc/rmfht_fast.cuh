@@ -1392,7 +1392,11 @@ __host__ __device__ constexpr size_t smem_bytes2(int nwarps) {
 // cap) whose LLR copies and scratch fit in 227 KB of shared memory
 template <int R, int MM, int L>
 __host__ __device__ constexpr int fast_warps() {
+#ifdef RMFHT_FAST_WARPS_MAX
+    int w = RMFHT_FAST_WARPS_MAX;  // A/B builds only (tools/build_variant.py)
+#else
     int w = 32;
+#endif
     while (w > 4 && smem_bytes2<R, MM, L>(w) > 227 * 1024) w -= 4;
     return w;
 }
