@@ -1407,7 +1407,12 @@ __host__ __device__ constexpr int fast_warps() {
 // instruction stream).
 // PM: permutations (p-FHT-FSCL); false = FHT-FSC (L = 1, identity maps)
 template <int R, int MM, int L, bool PM = true>
-__global__ void __launch_bounds__(32 * fast_warps<R, MM, L>(), 1) decode_kernel2(rmfht::Params<float> prm, AttHdr* hdr, u64* bitsout) {
+#ifdef RMFHT_FAST_LB_WARPS
+#define RMFHT_KERNEL2_LB (32 * RMFHT_FAST_LB_WARPS)  // A/B builds only: register cap of a larger CTA
+#else
+#define RMFHT_KERNEL2_LB (32 * fast_warps<R, MM, L>())
+#endif
+__global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Params<float> prm, AttHdr* hdr, u64* bitsout) {
     using C = Cfg<R, MM, L>;
     using WS = WS2<R, MM, L>;
     using LV = Lv<MM, C::LPP>;

@@ -74,27 +74,6 @@ RMFHT_HD int expand_one(const uint16_t* raw, int mn, int mg, uint16_t* rec) {
     return 0;
 }
 
-// Gauss-Jordan over GF(2) with compile-time size on augmented rows: t[r]
-// holds row r of T in bits 0..15 and row r of the identity in bits 16..31, so
-// one XOR is one row operation on [T | I].  Swap-free: a missing pivot is
-// repaired by adding a later row that has it.  On success t[r] >> 16 is row r
-// of T^-1.
-template <int MN>
-RMFHT_HD bool gj_inverse_aug(unsigned (&t)[MN]) {
-#pragma unroll
-    for (int c = 0; c < MN; c++) {
-        const unsigned bit = 1u << c;
-#pragma unroll
-        for (int r = c + 1; r < MN; r++)
-            if (~t[c] & t[r] & bit) t[c] ^= t[r];
-        if (!(t[c] & bit)) return false;
-#pragma unroll
-        for (int r = 0; r < MN; r++)
-            if (r != c && (t[r] & bit)) t[r] ^= t[c];
-    }
-    return true;
-}
-
 // Table semantics (host and device): slot s of (frame f, attempt a) holds a
 // map drawn from its own counter-based stream keyed by (seed, f, a, s), so a
 // frame's maps do not depend on the batch or the thread that draws them.
@@ -126,75 +105,91 @@ struct Word16 {
 };
 
 // Uniform (A, b) in GL(MN,2) x F_2^MN — the distribution of the reference's
-// rejection sampler (automorphism.py:127-161) — drawn column by column: each
-// column is uniform over the vectors outside the span of the previous ones
-// (redrawn while inside it), so every invertible A has probability 1/|GL|.
-// The span test reduces the candidate against a semi-echelon basis (u_j with
-// distinct pivot bits p_j, each later u free of earlier pivots).  Columns are
-// drawn directly because the device record stores columns; Gauss-Jordan on
-// T = A^T then gives the rows of (A^T)^-1 = the columns of A^-1.
+// rejection sampler (automorphism.py:127-161) — drawn column by column, each
+// column uniform over the vectors outside the span of the previous ones, so
+// every invertible A has probability 1/|GL|.
+//
+// The span is kept as a REDUCED echelon basis u_j (pivot coordinate p_j:
+// u_j has bit p_j set and every other pivot bit clear).  A vector x is
+// written uniquely as x = r ^ sum_{j: s_j} u_j with r supported on the free
+// (non-pivot) coordinates and s_j = bit p_j of x, so x is outside the span
+// iff r != 0, and a uniform m-bit v gives a uniform column outside the span
+// as r = v & free (redrawn while 0; the last column's single free bit is
+// forced), s = the pivot bits of v.  The redraw loop is a mask test, so
+// lanes that redraw do not hold the warp in a reduction loop.
+//
+// Each basis word also carries, in bits 16.., its coefficients over the
+// columns drawn so far (A * coef_j = u_j): the new u_i = r has coef
+// e_i ^ sum_{j: s_j} coef_j, and eliminating p_i from the earlier u_j XORs
+// both halves.  After MN columns the u_j are the unit vectors e_{p_j}, so
+// A^-1 e_{p_j} = coef_j: the columns of A^-1 without a Gauss-Jordan pass.
 template <int MN>
 RMFHT_HD void draw_map(uint64_t key, unsigned (&cols)[MN], unsigned (&icols)[MN], unsigned& b) {
     constexpr unsigned mask = (1u << MN) - 1u;
     Word16 rs(key);
-    unsigned u[MN], piv[MN];
+    unsigned ub[MN], pv[MN];  // basis word (u | coef << 16), pivot bit
+    unsigned pivm = 0u;
 #pragma unroll
     for (int i = 0; i < MN; i++) {
-        for (;;) {
-            const unsigned v = rs.next() & mask;
-            unsigned x = v;
+        unsigned v, r;
+        do {
+            v = rs.next() & mask;
+            r = (i == MN - 1) ? (mask & ~pivm) : (v & ~pivm);
+        } while (r == 0u);
+        unsigned t = 0u;
 #pragma unroll
-            for (int j = 0; j < i; j++)
-                if (x & piv[j]) x ^= u[j];
-            if (x) {
-                cols[i] = v;
-                u[i] = x;
-                piv[i] = x & (0u - x);
-                break;
-            }
-        }
+        for (int j = 0; j < i; j++)
+            if (v & pv[j]) t ^= ub[j];
+        cols[i] = r ^ (t & 0xffffu);
+        ub[i] = (r | (1u << (16 + i))) ^ (t & 0xffff0000u);
+        pv[i] = r & (0u - r);
+        pivm |= pv[i];
+#pragma unroll
+        for (int j = 0; j < i; j++)
+            if (ub[j] & pv[i]) ub[j] ^= ub[i];
     }
     b = rs.next() & mask;
-    unsigned t[MN];
 #pragma unroll
-    for (int k = 0; k < MN; k++) t[k] = cols[k] | (1u << (16 + k));
-    gj_inverse_aug<MN>(t);  // A is invertible by construction
+    for (int k = 0; k < MN; k++) {
+        unsigned c = 0u;
 #pragma unroll
-    for (int k = 0; k < MN; k++) icols[k] = t[k] >> 16;
+        for (int j = 0; j < MN; j++)
+            if ((ub[j] >> k) & 1u) c = ub[j] >> 16;
+        icols[k] = c;
+    }
 }
 
-// runtime-size draw_map (rare slots: map sizes below m-2)
+// runtime-size draw_map (rare slots: map sizes below m-2); same draws
 RMFHT_HD void draw_map_rt(uint64_t key, int mn, unsigned* cols, unsigned* icols, unsigned& b) {
     const unsigned mask = (1u << mn) - 1u;
     Word16 rs(key);
-    unsigned u[16], piv[16], t[16];
+    unsigned ub[16], pv[16];
+    unsigned pivm = 0u;
     for (int i = 0; i < mn; i++) {
-        for (;;) {
-            const unsigned v = rs.next() & mask;
-            unsigned x = v;
-            for (int j = 0; j < i; j++)
-                if (x & piv[j]) x ^= u[j];
-            if (x) {
-                cols[i] = v;
-                u[i] = x;
-                piv[i] = x & (0u - x);
-                break;
-            }
-        }
+        unsigned v, r;
+        do {
+            v = rs.next() & mask;
+            r = (i == mn - 1) ? (mask & ~pivm) : (v & ~pivm);
+        } while (r == 0u);
+        unsigned t = 0u;
+        for (int j = 0; j < i; j++)
+            if (v & pv[j]) t ^= ub[j];
+        cols[i] = r ^ (t & 0xffffu);
+        ub[i] = (r | (1u << (16 + i))) ^ (t & 0xffff0000u);
+        pv[i] = r & (0u - r);
+        pivm |= pv[i];
+        for (int j = 0; j < i; j++)
+            if (ub[j] & pv[i]) ub[j] ^= ub[i];
     }
     b = rs.next() & mask;
-    for (int k = 0; k < mn; k++) t[k] = cols[k] | (1u << (16 + k));
-    for (int c = 0; c < mn; c++) {
-        const unsigned bit = 1u << c;
-        for (int r = c + 1; r < mn; r++)
-            if (~t[c] & t[r] & bit) t[c] ^= t[r];
-        for (int r = 0; r < mn; r++)
-            if (r != c && (t[r] & bit)) t[r] ^= t[c];
+    for (int k = 0; k < mn; k++) {
+        unsigned c = 0u;
+        for (int j = 0; j < mn; j++)
+            if ((ub[j] >> k) & 1u) c = ub[j] >> 16;
+        icols[k] = c;
     }
-    for (int k = 0; k < mn; k++) icols[k] = t[k] >> 16;
 }
 
-// A^-1 b = XOR of the columns of A^-1 selected by b
 template <int MN>
 RMFHT_HD unsigned inv_shift(const unsigned (&icols)[MN], unsigned b) {
     unsigned v = 0;

@@ -142,3 +142,35 @@ def test_counter_sampler_batch_independent_and_identity_root():
     assert not np.any(np.all(raw[:, 1:, :, :] == ident, axis=-1))
     raw3, _ = plan.sample(10, seed=6, frame0=0)
     assert not np.array_equal(raw3[:, 1:], raw[:, 1:])
+
+
+def test_counter_sampler_records_hold_the_inverse():
+    """The sampler reads A^-1 off its reduced echelon basis (no Gauss-Jordan):
+    every record's inverse columns, and c = A^-1 b, must invert (A, b); the
+    raw rows must be the transpose of the record's columns.  Every map size
+    of RM(3,7) L=8 (7 and 6 variables) and RM(2,9)."""
+    from paper_2108_12550_b200.decoder import Plan
+
+    def gf2_mul(cols_a, cols_b, m):  # columns of A.B
+        out = []
+        for cb in cols_b:
+            v = 0
+            for k in range(m):
+                if (cb >> k) & 1:
+                    v ^= cols_a[k]
+            out.append(v)
+        return out
+
+    for (r, m, L, M) in [(3, 7, 8, 3), (2, 9, 4, 3)]:
+        plan = Plan(r, m, L, M, True, "f32")
+        raw, rec = plan.sample(6, seed=13, identity_root=False)
+        for f in range(6):
+            for a in range(M):
+                for s, mn in enumerate(plan.sizes):
+                    rr = [int(x) for x in rec[f, a, s]]
+                    cols, b, icols, c = rr[:m], rr[m], rr[m + 1:2 * m + 1], rr[2 * m + 1]
+                    assert not any(cols[mn:]) and not any(icols[mn:])
+                    assert gf2_mul(cols[:mn], icols[:mn], mn) == [1 << k for k in range(mn)]
+                    assert gf2_mul(icols[:mn], [b], mn)[0] == c
+                    rows = [sum(((cols[k] >> i) & 1) << k for k in range(mn)) for i in range(mn)]
+                    assert [int(x) for x in raw[f, a, s, :mn]] == rows and int(raw[f, a, s, m]) == b
