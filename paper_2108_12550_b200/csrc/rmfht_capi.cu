@@ -52,9 +52,9 @@ struct SampleArgs {
     signed char sizes[128];
 };
 
-// one record (2MG+2 uint16 = MG+1 words) built in registers
-template <int MN, int MG>
-__device__ __forceinline__ void draw_store(uint64_t key, uint32_t* o) {
+// one record (2MG+2 uint16 = MG+1 words) built in registers, word w handed to put(w, value)
+template <int MN, int MG, typename Put>
+__device__ __forceinline__ void draw_store(uint64_t key, Put&& put) {
     unsigned cols[MN], icols[MN], b;
     rmfht_maps::draw_map<MN>(key, cols, icols, b);
     // record halves: cols of A (MG), b, cols of A^-1 (MG), A^-1 b
@@ -67,64 +67,87 @@ __device__ __forceinline__ void draw_store(uint64_t key, uint32_t* o) {
     h[MG] = b;
     h[2 * MG + 1] = rmfht_maps::inv_shift<MN>(icols, b);
 #pragma unroll
-    for (int w = 0; w <= MG; w++) o[w] = h[2 * w] | (h[2 * w + 1] << 16);
+    for (int w = 0; w <= MG; w++) put(w, h[2 * w] | (h[2 * w + 1] << 16));
 }
 
 // slots below MG-2 variables (r >= 5)
 template <int MG>
-__device__ __noinline__ void draw_store_rt(uint64_t key, int mn, uint16_t* o) {
+__device__ __noinline__ void draw_store_rt(uint64_t key, int mn, uint32_t* o) {
     unsigned cols[16], icols[16], b;
     rmfht_maps::draw_map_rt(key, mn, cols, icols, b);
-    unsigned cinv = 0;
+    unsigned cinv = 0, h[2 * MG + 2];
     for (int k = 0; k < MG; k++) {
-        o[k] = (uint16_t)(k < mn ? cols[k] : 0u);
-        o[MG + 1 + k] = (uint16_t)(k < mn ? icols[k] : 0u);
+        h[k] = k < mn ? cols[k] : 0u;
+        h[MG + 1 + k] = k < mn ? icols[k] : 0u;
         if (k < mn && ((b >> k) & 1u)) cinv ^= icols[k];
     }
-    o[MG] = (uint16_t)b;
-    o[2 * MG + 1] = (uint16_t)cinv;
+    h[MG] = b;
+    h[2 * MG + 1] = cinv;
+    for (int w = 0; w <= MG; w++) o[w] = h[2 * w] | (h[2 * w + 1] << 16);
 }
 
-// One thread per (frame, attempt, slot); a warp takes one slot of 32
-// consecutive (frame, attempt) items, so its lanes draw maps of one size.
+// A CTA draws the records of G consecutive (frame, attempt) items: warp w
+// takes slots w, w + 8, ... with one lane per item (a warp's lanes draw maps
+// of one size), the records are staged in shared memory in their global
+// order (one pad word per 32 against bank conflicts) and leave in contiguous
+// 32-bit stores — the item-major record layout made per-lane stores
+// S x 40 B apart, which throttled the store pipe.
 template <int MG>
-__global__ void __launch_bounds__(256) sample_kernel(SampleArgs a, uint16_t* rec) {
+__global__ void __launch_bounds__(256) sample_kernel(SampleArgs a, uint32_t* rec, int G) {
+    extern __shared__ uint32_t stage[];
+    constexpr int W = MG + 1;  // words per record
     const long long items = a.B * (long long)a.M;
-    const long long groups = (items + 31) / 32;
-    const int lane = threadIdx.x & 31;
-    auto one = [&](int s, long long item, long long f, int at) {
-        uint16_t* o = rec + ((size_t)item * a.S + s) * (2 * MG + 2);
-        const int mn = a.sizes[s];
-        if (a.identity_root && at == 0 && s < a.L) {
-            rmfht_maps::write_identity(mn, MG, nullptr, o);
-            return;
+    const int S = a.S, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long groups = (items + G - 1) / G;
+    for (long long g = blockIdx.x; g < groups; g += gridDim.x) {
+        const long long item0 = g * G;
+        const int nit = (int)(items - item0 < G ? items - item0 : G);
+        if (lane < nit) {
+            const long long item = item0 + lane;
+            long long f;
+            int at;
+            if (item < (1LL << 31)) {
+                const unsigned q = (unsigned)item / (unsigned)a.M;
+                f = q;
+                at = (int)((unsigned)item - q * (unsigned)a.M);
+            } else {
+                f = item / a.M;
+                at = (int)(item % a.M);
+            }
+            f += a.frame0;
+            for (int s = warp; s < S; s += 8) {
+                const unsigned o0 = (unsigned)(lane * S + s) * W;
+                auto put = [&](int w, unsigned v) {
+                    const unsigned o = o0 + w;
+                    stage[o + (o >> 5)] = v;
+                };
+                const int mn = a.sizes[s];
+                if (a.identity_root && at == 0 && s < a.L) {
+                    unsigned h[2 * MG + 2];
+#pragma unroll
+                    for (int k = 0; k < 2 * MG + 2; k++) h[k] = 0u;
+                    for (int k = 0; k < mn; k++) h[k] = h[MG + 1 + k] = 1u << k;
+#pragma unroll
+                    for (int w = 0; w < W; w++) put(w, h[2 * w] | (h[2 * w + 1] << 16));
+                    continue;
+                }
+                const uint64_t key = rmfht_maps::slot_key(a.seed, f, at, s);
+                if (mn == MG) draw_store<MG, MG>(key, put);
+                else if (mn == MG - 1 && MG > 1) draw_store<(MG > 1 ? MG - 1 : 1), MG>(key, put);
+                else if (mn == MG - 2 && MG > 2) draw_store<(MG > 2 ? MG - 2 : 1), MG>(key, put);
+                else {
+                    uint32_t t[W];
+                    draw_store_rt<MG>(key, mn, t);
+#pragma unroll
+                    for (int w = 0; w < W; w++) put(w, t[w]);
+                }
+            }
         }
-        const uint64_t key = rmfht_maps::slot_key(a.seed, f, at, s);
-        uint32_t* o32 = reinterpret_cast<uint32_t*>(o);
-        if (mn == MG) draw_store<MG, MG>(key, o32);
-        else if (mn == MG - 1 && MG > 1) draw_store<(MG > 1 ? MG - 1 : 1), MG>(key, o32);
-        else if (mn == MG - 2 && MG > 2) draw_store<(MG > 2 ? MG - 2 : 1), MG>(key, o32);
-        else draw_store_rt<MG>(key, mn, o);
-    };
-    if (groups * a.S < (1LL << 31)) {
-        // 32-bit index arithmetic (the 64-bit divisions cost as much as a map's RNG)
-        const unsigned total = (unsigned)(groups * a.S), S = (unsigned)a.S, M = (unsigned)a.M;
-        const unsigned nw = gridDim.x * blockDim.x / 32;
-        for (unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) / 32; w < total; w += nw) {
-            const unsigned g = w / S, s = w - g * S;
-            const unsigned item = g * 32 + lane;
-            if (item >= (unsigned)items) continue;
-            const unsigned fr = item / M;
-            one((int)s, (long long)item, a.frame0 + fr, (int)(item - fr * M));
-        }
-        return;
-    }
-    const long long nwarps = (long long)gridDim.x * blockDim.x / 32;
-    for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; w < groups * a.S; w += nwarps) {
-        const int s = (int)(w % a.S);
-        const long long item = (w / a.S) * 32 + lane;
-        if (item >= items) continue;
-        one(s, item, a.frame0 + item / a.M, (int)(item % a.M));
+        __syncthreads();
+        uint32_t* dst = rec + (size_t)item0 * S * W;
+        const int T = nit * S * W;
+        for (int o = threadIdx.x; o < T; o += blockDim.x) dst[o] = stage[o + (o >> 5)];
+        __syncthreads();
     }
 }
 
@@ -283,14 +306,21 @@ int rmfht_sample_maps_device(const rmfht_plan* p, uint64_t seed, long long frame
     a.m = p->m;
     a.identity_root = identity_root;
     for (int s = 0; s < p->S; s++) a.sizes[s] = (signed char)p->sizes[s];
-    const long long warps = (B * (long long)p->M + 31) / 32 * p->S;
-    long long blocks = (warps * 32 + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (reinterpret_cast<uintptr_t>(d_rec) & 3u) return fail(RMFHT_EVALUE, "d_rec must be 4-byte aligned");
+    // items per CTA group: 32 (one per lane) unless the staged records exceed 48 KB
+    const int W = p->m + 1;
+    int G = 32;
+    auto stage_bytes = [&](int g) { const size_t t = (size_t)g * p->S * W; return (t + t / 32 + 1) * 4; };
+    while (G > 1 && stage_bytes(G) > 48 * 1024) G /= 2;
+    const long long groups = (B * (long long)p->M + G - 1) / G;
+    long long blocks = groups < 148 * 16 ? groups : 148 * 16;
+    const size_t smem = stage_bytes(G);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint32_t* d_rec32 = reinterpret_cast<uint32_t*>(d_rec);
     switch (p->m) {
 #define RMFHT_SK(K) \
     case K:         \
-        sample_kernel<K><<<(unsigned)blocks, 256, 0, st>>>(a, d_rec); \
+        sample_kernel<K><<<(unsigned)blocks, 256, smem, st>>>(a, d_rec32, G); \
         break;
         RMFHT_SK(2) RMFHT_SK(3) RMFHT_SK(4) RMFHT_SK(5) RMFHT_SK(6) RMFHT_SK(7) RMFHT_SK(8) RMFHT_SK(9)
         RMFHT_SK(10) RMFHT_SK(11) RMFHT_SK(12) RMFHT_SK(13) RMFHT_SK(14)
