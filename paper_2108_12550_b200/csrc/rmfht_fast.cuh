@@ -375,6 +375,123 @@ __device__ __noinline__ void fht_fallback(WS2<R, MM, L>* wsp_, int lane, float l
         __syncwarp();
     }
 
+// Exact list path of fht_node (cold: a same-path pm collision among the
+// pool's top L, or more than kCap candidates): per-path top-K by (|w| desc,
+// bin asc) (fht_decode.py:116), then the pool ranked by the 64-bit key
+// (pm, source path, bin) (:120).  Out of line so the hot node code stays
+// compact in the instruction cache.
+template <int R, int MM, int L, int SS>
+__device__ __noinline__ void fht_exact(WS2<R, MM, L>* wsp_, int lane, u64 mask64, int cnt, int total, float pmp,
+                                       float llrabs) {
+    using C = Cfg<R, MM, L>;
+    using LV = Lv<SS, C::LPP>;
+    using FL = FhtLayout<R, MM, L, SS>;
+    constexpr int n = LV::n, V = LV::V, K = cmin(L, n);
+    using MaskT = typename std::conditional<(V > 32), u64, u32>::type;
+    auto& ws = *wsp_;
+    const int p = lane / C::LPP, u = lane % C::LPP;
+    const int tw = FL::twist(p);
+    const MaskT mask = (MaskT)mask64;
+    (void)n;
+    // candidates per path (for the per-path top-K rule, fht_decode.py:116) and
+    // each lane's position in the warp list (inclusive prefix sum)
+    int pcnt = cnt;
+#pragma unroll
+    for (int off = 1; off < LV::act; off <<= 1) pcnt += __shfl_xor_sync(kFull, pcnt, off);
+    int incl = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(kFull, incl, off);
+        if (lane >= off) incl += t;
+    }
+    if (total <= kCap) {
+        const bool over = __any_sync(kFull, pcnt > K);
+        RMFHT_STAT(SS * 8 + 2);
+        if (over) RMFHT_STAT(SS * 8 + 5);
+        int pos = incl - cnt;
+        // this path's candidates occupy [pstart, pstart + pcnt) (lane order)
+        const int pstart = __shfl_sync(kFull, incl - cnt, p * C::LPP);
+        if (u == 0) {
+            ws.cp[p] = pstart;
+            ws.celig[p] = pcnt;
+        }
+        MaskT mk = mask;
+        while (mk) {
+            const int k = sizeof(MaskT) == 8 ? __ffsll((long long)mk) - 1 : __ffs((int)mk) - 1;
+            mk &= mk - 1;
+            const float v = ws.wspk(lane, k, tw);
+            const float a = fabsf(v);
+            const int bin = FL::bin(k, u);
+            const float pmc = pmp + 0.5f * (llrabs - a);  // :119
+            u32 kb = __float_as_uint(pmc);
+            kb ^= (kb >> 31) ? 0xffffffffu : 0x80000000u;  // order-preserving for any sign
+            ws.ckey[pos] = ((u64)kb << 32) | ((u32)p << 16) | (u32)bin;
+            ws.ca[pos] = a;
+            ws.cw[pos] = v;
+            pos++;
+        }
+        if (lane < 4 && total + lane < ((total + 3) & ~3)) ws.ckey[total + lane] = ~0ull;  // pad to 4
+        __syncwarp();
+        if (over) {
+            // a path with more than K candidates: keep only its top-K by
+            // (|w| desc, bin asc); the rest leave the pool
+            bool kill[2] = {false, false};
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int i = lane + 32 * h;
+                if (i < total) {
+                    const u64 ki = ws.ckey[i];
+                    const int pi = (int)((ki >> 16) & 0xffff), bi = (int)(ki & 0xffff);
+                    const int j0 = ws.cp[pi], j1 = j0 + ws.celig[pi];
+                    if (j1 - j0 > K) {
+                        const float ai = ws.ca[i];
+                        int rp = 0;
+#pragma unroll 1
+                        for (int j = j0; j < j1; j++) {
+                            const float aj = ws.ca[j];
+                            rp += aj > ai || (aj == ai && (int)(ws.ckey[j] & 0xffff) < bi);
+                        }
+                        kill[h] = rp >= K;
+                    }
+                }
+            }
+            __syncwarp();
+            if (kill[0]) ws.ckey[lane] = ~0ull;
+            if (kill[1]) ws.ckey[lane + 32] = ~0ull;
+            __syncwarp();
+        }
+        // pool: rank by (pm, source path, bin) (:120)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int i = lane + 32 * h;
+            if (h == 1 && total <= 32) break;
+            const u64 ki = i < total ? ws.ckey[i] : ~0ull;
+            if (ki != ~0ull) {
+                int rank = 0;
+                const int tot4 = (total + 3) & ~3;
+#pragma unroll 1
+                for (int j = 0; j < tot4; j += 4) {
+                    const ulonglong2 k01 = *reinterpret_cast<const ulonglong2*>(&ws.ckey[j]);
+                    const ulonglong2 k23 = *reinterpret_cast<const ulonglong2*>(&ws.ckey[j + 2]);
+                    rank += (k01.x < ki) + (k01.y < ki) + (k23.x < ki) + (k23.y < ki);
+                }
+                if (rank < L) {
+                    u32 kb = (u32)(ki >> 32);
+                    kb ^= (kb >> 31) ? 0x80000000u : 0xffffffffu;
+                    ws.sel_src[rank] = (int)((ki >> 16) & 0xffff);
+                    ws.sel_bin[rank] = (int)(ki & 0xffff);
+                    ws.sel_w[rank] = ws.cw[i];
+                    ws.sel_pm[rank] = __uint_as_float(kb);
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        RMFHT_STAT(SS * 8 + 3);
+        fht_fallback<R, MM, L, SS>(&ws, lane, llrabs);
+    }
+}
+
 // ------------------------------------------- FHT node (RR == 1) ---------
 // fhtl (fht_decode.py:101-126) on all L paths (P == L invariant of
 // p-FHT-FSCL).  x[] is this lane's part of its path's node vector.
@@ -612,105 +729,7 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
         RMFHT_STAT(SS * 8 + 6);
         if (exact_needed) RMFHT_STAT(SS * 8 + 7);
     }
-    if (exact_needed) {
-    // candidates per path (for the per-path top-K rule, fht_decode.py:116) and
-    // each lane's position in the warp list (inclusive prefix sum)
-    int pcnt = cnt;
-#pragma unroll
-    for (int off = 1; off < LV::act; off <<= 1) pcnt += __shfl_xor_sync(kFull, pcnt, off);
-    int incl = cnt;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const int t = __shfl_up_sync(kFull, incl, off);
-        if (lane >= off) incl += t;
-    }
-    if (total <= kCap) {
-        const bool over = __any_sync(kFull, pcnt > K);
-        RMFHT_STAT(SS * 8 + 2);
-        if (over) RMFHT_STAT(SS * 8 + 5);
-        int pos = incl - cnt;
-        // this path's candidates occupy [pstart, pstart + pcnt) (lane order)
-        const int pstart = __shfl_sync(kFull, incl - cnt, p * C::LPP);
-        if (u == 0) {
-            ws.cp[p] = pstart;
-            ws.celig[p] = pcnt;
-        }
-        MaskT mk = mask;
-        while (mk) {
-            const int k = sizeof(MaskT) == 8 ? __ffsll((long long)mk) - 1 : __ffs((int)mk) - 1;
-            mk &= mk - 1;
-            const float v = ws.wspk(lane, k, tw);
-            const float a = fabsf(v);
-            const int bin = FL::bin(k, u);
-            const float pmc = pmp + 0.5f * (llrabs - a);  // :119
-            u32 kb = __float_as_uint(pmc);
-            kb ^= (kb >> 31) ? 0xffffffffu : 0x80000000u;  // order-preserving for any sign
-            ws.ckey[pos] = ((u64)kb << 32) | ((u32)p << 16) | (u32)bin;
-            ws.ca[pos] = a;
-            ws.cw[pos] = v;
-            pos++;
-        }
-        if (lane < 4 && total + lane < ((total + 3) & ~3)) ws.ckey[total + lane] = ~0ull;  // pad to 4
-        __syncwarp();
-        if (over) {
-            // a path with more than K candidates: keep only its top-K by
-            // (|w| desc, bin asc); the rest leave the pool
-            bool kill[2] = {false, false};
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-                const int i = lane + 32 * h;
-                if (i < total) {
-                    const u64 ki = ws.ckey[i];
-                    const int pi = (int)((ki >> 16) & 0xffff), bi = (int)(ki & 0xffff);
-                    const int j0 = ws.cp[pi], j1 = j0 + ws.celig[pi];
-                    if (j1 - j0 > K) {
-                        const float ai = ws.ca[i];
-                        int rp = 0;
-#pragma unroll 1
-                        for (int j = j0; j < j1; j++) {
-                            const float aj = ws.ca[j];
-                            rp += aj > ai || (aj == ai && (int)(ws.ckey[j] & 0xffff) < bi);
-                        }
-                        kill[h] = rp >= K;
-                    }
-                }
-            }
-            __syncwarp();
-            if (kill[0]) ws.ckey[lane] = ~0ull;
-            if (kill[1]) ws.ckey[lane + 32] = ~0ull;
-            __syncwarp();
-        }
-        // pool: rank by (pm, source path, bin) (:120)
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int i = lane + 32 * h;
-            if (h == 1 && total <= 32) break;
-            const u64 ki = i < total ? ws.ckey[i] : ~0ull;
-            if (ki != ~0ull) {
-                int rank = 0;
-                const int tot4 = (total + 3) & ~3;
-#pragma unroll 1
-                for (int j = 0; j < tot4; j += 4) {
-                    const ulonglong2 k01 = *reinterpret_cast<const ulonglong2*>(&ws.ckey[j]);
-                    const ulonglong2 k23 = *reinterpret_cast<const ulonglong2*>(&ws.ckey[j + 2]);
-                    rank += (k01.x < ki) + (k01.y < ki) + (k23.x < ki) + (k23.y < ki);
-                }
-                if (rank < L) {
-                    u32 kb = (u32)(ki >> 32);
-                    kb ^= (kb >> 31) ? 0x80000000u : 0xffffffffu;
-                    ws.sel_src[rank] = (int)((ki >> 16) & 0xffff);
-                    ws.sel_bin[rank] = (int)(ki & 0xffff);
-                    ws.sel_w[rank] = ws.cw[i];
-                    ws.sel_pm[rank] = __uint_as_float(kb);
-                }
-            }
-        }
-        __syncwarp();
-    } else {
-        RMFHT_STAT(SS * 8 + 3);
-        fht_fallback<R, MM, L, SS>(&cx.ws, lane, llrabs);
-    }
-    }
+    if (exact_needed) fht_exact<R, MM, L, SS>(&cx.ws, lane, (u64)mask, cnt, total, pmp, llrabs);
     }
     // survivors: pm, lineage; my group's codeword bits
     if (lane < L) {
