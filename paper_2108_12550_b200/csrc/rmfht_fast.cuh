@@ -699,8 +699,10 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
         lane_best(rem, hi, lo);
         // picks come in ascending pm order, so a same-path pm collision that
         // matters (a remaining candidate with the pm of a pick) can only be at
-        // the last pick's pm: track the paths picked at that pm
-        u32 hlast = 0xffffffffu, lastpaths = 0u;
+        // the last pick's pm: each lane remembers the key of its own latest
+        // pick, and the paths picked at the last pm are one ballot after the
+        // rounds
+        u32 hlast = 0xffffffffu, mine = 0xffffffffu;
 #pragma unroll 1
         for (int r = 0; r < L; r++) {
             const u32 hmin = __reduce_min_sync(kFull, hi);
@@ -710,8 +712,6 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
                 const u32 lmin = __reduce_min_sync(kFull, hi == hmin ? lo : 0xffffffffu);
                 wl = __ffs(__ballot_sync(kFull, hi == hmin && lo == lmin)) - 1;
             }
-            const u32 pbit = 1u << (wl / C::LPP);
-            lastpaths = hmin == hlast ? (lastpaths | pbit) : pbit;
             hlast = hmin;
             if (lane == wl) {
                 const int bin = (int)(lo & 0xffffu);
@@ -720,11 +720,14 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
                 ws.sel_bin[r] = bin;
                 ws.sel_w[r] = ws.wspk(lane, k, tw);
                 ws.sel_pm[r] = key_float(hmin);
+                mine = hmin;
                 rem &= ~((MaskT)1 << k);
                 lane_best(rem, hi, lo);
             }
         }
-        exact_needed = __any_sync(kFull, hi == hlast && ((lastpaths >> p) & 1u));
+        const u32 lastb = __ballot_sync(kFull, mine == hlast);  // lanes that picked at the last pm
+        const bool path_last = ((lastb >> (p * C::LPP)) & GBITS) != 0u;
+        exact_needed = __any_sync(kFull, hi == hlast && path_last);
         __syncwarp();
         RMFHT_STAT(SS * 8 + 6);
         if (exact_needed) RMFHT_STAT(SS * 8 + 7);
