@@ -618,7 +618,18 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
     const float theta = th0 - (fabsf(th0) + llrabs + fabsf(tau) + fabsf(pmp)) * 9.5367431640625e-07f - 1e-30f;
     using MaskT = typename std::conditional<(V > 32), u64, u32>::type;
     MaskT mask;
-    {
+    if constexpr (sizeof(MaskT) == 4) {
+        // one compare and one predicated OR per element
+        u32 m0 = 0u, m1 = 0u;
+#pragma unroll
+        for (int k = 0; k < V; k++) {
+            if (fabsf(w[k]) >= theta) {
+                if (k & 1) m1 |= 1u << k;
+                else m0 |= 1u << k;
+            }
+        }
+        mask = act ? (m0 | m1) : 0u;
+    } else {
         MaskT t[V];
 #pragma unroll
         for (int k = 0; k < V; k++) t[k] = fabsf(w[k]) >= theta ? ((MaskT)1 << k) : (MaskT)0;
@@ -648,26 +659,26 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
     if (total == L && __all_sync(kFull, ((bal >> (p * C::LPP)) & GBITS) != 0u)) {
         RMFHT_STAT(SS * 8 + 1);
         // the pool is the L path maxima ordered by (pm, source slot) (:116-120)
-        const int owner = __ffs((bal >> (p * C::LPP)) & GBITS) - 1;
-        int mybin = 0;
-        float myw = 0.f;
+        int rank = 0;
+        if constexpr (C::LPP >= L) {
+            // lane u < L of every group compares its path with path u: one
+            // shuffle and one ballot give each path its rank
+            const float cq = __shfl_sync(kFull, cbest, (u < L ? u : 0) * C::LPP);
+            const bool before = u < L && ((cq < cbest) || (cq == cbest && u < p));
+            rank = __popc((__ballot_sync(kFull, before) >> (p * C::LPP)) & ((1u << L) - 1u));
+        } else {
+#pragma unroll
+            for (int q = 0; q < L; q++) {
+                const float cq = __shfl_sync(kFull, cbest, q * C::LPP);
+                rank += (cq < cbest) || (cq == cbest && q < p);
+            }
+        }
+        // the one lane of each path holding a candidate (its maximum) records it
         if (cnt > 0) {
             const int k = (sizeof(MaskT) == 8 ? __ffsll((long long)mask) : __ffs((int)mask)) - 1;
-            mybin = FL::bin(k, u);
-            myw = ws.wspk(lane, k, tw);
-        }
-        const int bin = __shfl_sync(kFull, mybin, p * C::LPP + owner);
-        const float wv = __shfl_sync(kFull, myw, p * C::LPP + owner);
-        int rank = 0;
-#pragma unroll
-        for (int q = 0; q < L; q++) {
-            const float cq = __shfl_sync(kFull, cbest, q * C::LPP);
-            rank += (cq < cbest) || (cq == cbest && q < p);
-        }
-        if (u == 0) {
             ws.sel_src[rank] = p;
-            ws.sel_bin[rank] = bin;
-            ws.sel_w[rank] = wv;
+            ws.sel_bin[rank] = FL::bin(k, u);
+            ws.sel_w[rank] = ws.wspk(lane, k, tw);
             ws.sel_pm[rank] = cbest;
         }
         __syncwarp();
