@@ -98,12 +98,34 @@ struct Lv {
 // an affine map in device-record layout (rmfht.h): columns of A, b, columns
 // of A^-1, A^-1 b — read in place from the item's record buffer
 template <int MM>
-struct MapR {
+struct alignas(4) MapR {
     uint16_t col[MM];
     uint16_t b;
     uint16_t icol[MM];
     uint16_t c;
 };
+
+// A^-1 x of a record (x: m-bit): the columns come in as 32-bit words (half
+// word MM + 1 + k of the record is icol[k]) and every set bit of x XORs a
+// whole word into the low- or high-half accumulator
+template <int MM>
+__device__ __forceinline__ uint32_t icol_apply(const MapR<MM>& mp, uint32_t x) {
+    constexpr int W0 = (MM + 1) >> 1, W1 = (2 * MM) >> 1;
+    const uint32_t* wp = reinterpret_cast<const uint32_t*>(&mp);
+    uint32_t wv[W1 - W0 + 1];
+#pragma unroll
+    for (int i = 0; i <= W1 - W0; i++) wv[i] = wp[W0 + i];
+    uint32_t lo = 0u, hi = 0u;
+#pragma unroll
+    for (int k = 0; k < MM; k++) {
+        const int h = MM + 1 + k;
+        if ((x >> k) & 1u) {
+            if (h & 1) hi ^= wv[(h >> 1) - W0];
+            else lo ^= wv[(h >> 1) - W0];
+        }
+    }
+    return (lo ^ (hi >> 16)) & 0xffffu;
+}
 
 // per-warp shared scratch
 template <int R, int MM, int L>
@@ -1108,7 +1130,7 @@ __device__ __forceinline__ void perm_ext_root2(Ctx2<R, MM, L>& cx) {
     const int lane = cx.lane, base = ws.next_map;
     // pairing direction of each trial's composite: A_init^-1 (A_t^-1 e_{m-1})
     if (lane < 2 * L) {
-        const u32 d = lin_apply<MM>(ws.comp[lane % L].icol, (u32)cx.maps[base + lane].icol[MM - 1]);
+        const u32 d = icol_apply<MM>(ws.comp[lane % L], (u32)cx.maps[base + lane].icol[MM - 1]);
         ws.cb[lane] = (int)d;
     }
     __syncwarp();
@@ -1136,8 +1158,9 @@ __device__ __forceinline__ void perm_ext_root2(Ctx2<R, MM, L>& cx) {
             const int t = ws.ord[o];
             const MapR<MM>& tm = cx.maps[base + t];
             const MapR<MM>& im = ws.comp[t % L];
-            nv[q] = k < MM ? (uint16_t)lin_apply<MM>(im.icol, (u32)tm.icol[k])
-                           : (uint16_t)(lin_apply<MM>(im.icol, (u32)tm.c) ^ im.c);
+            // column k of the composite's inverse, or (k == MM) its shift
+            const u32 v = icol_apply<MM>(im, (u32)(k < MM ? tm.icol[k] : tm.c));
+            nv[q] = (uint16_t)(k < MM ? v : v ^ im.c);
         }
     }
     float npm = 0.f;

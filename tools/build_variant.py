@@ -6,7 +6,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2108_12550_b200 import _native
 name, extra = sys.argv[1], sys.argv[2:]
-out = os.path.join(ROOT, "tools", "_ab", name)
+out = os.path.join("/tmp", "rmfht_ab", name)  # objects stay here; only the .so travels
+os.makedirs(os.path.join(ROOT, "tools", "_ab"), exist_ok=True)
 os.makedirs(out, exist_ok=True)
 flags = [f for f in _native.NVCC_FLAGS if f not in ("-shared", "-lgomp")] + extra
 units = [("capi", "rmfht_capi.cu", []), ("gen", "rmfht_gen.cu", []), ("chan", "rmfht_chan.cu", []),
