@@ -705,16 +705,63 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
         }
         __syncwarp();
     } else {
-    // General case: L rounds of warp-wide minimum selection over the pool key
-    // (pm, source path, bin) (:120), each lane offering its best remaining
-    // candidate.  The per-path top-K cut (:116, K = L here) can only exclude
+    // General case, more than 32 candidates: L rounds of warp-wide minimum
+    // selection over the pool key (pm, source path, bin) (:120), each lane
+    // offering its best remaining candidate.  The per-path top-K cut (:116, K = L here) can only exclude
     // a pool top-L candidate X when a candidate Z of the same path has the
     // same pm but a larger |w| and a larger bin (a pm rounding collision);
     // every pick therefore checks that no other remaining candidate of its
     // path has its exact pm, and a collision hands the node to the exact
     // list path below.
     bool exact_needed = true;
-    if constexpr (K == L) {
+    if (K == L && total <= 32) {
+        // At most 32 candidates: list them (warp prefix sum of the counts),
+        // one per lane, and rank each by its 64-bit pool key (pm, source
+        // path, bin) (:120) against the whole list.  The per-path top-K cut
+        // (:116, K = L) can only remove a pool top-L candidate through a
+        // same-path pm collision at the L-th pick's pm (see the greedy
+        // selection below): checked after the ranks.
+        int incl = cnt;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int t = __shfl_up_sync(kFull, incl, off);
+            if (lane >= off) incl += t;
+        }
+        int pos = incl - cnt;
+        MaskT mk = mask;
+        while (mk) {
+            const int k = (sizeof(MaskT) == 8 ? __ffsll((long long)mk) : __ffs((int)mk)) - 1;
+            mk &= mk - 1;
+            const float pmc = pmp + 0.5f * (llrabs - fabsf(ws.wspk(lane, k, tw)));  // :119
+            ws.ckey[pos++] = ((u64)float_key(pmc) << 32) | ((u32)p << 16) | (u32)FL::bin(k, u);
+        }
+        if (lane < 4 && total + lane < ((total + 3) & ~3)) ws.ckey[total + lane] = ~0ull;  // pad to 4
+        __syncwarp();
+        const bool mine = lane < total;
+        const u64 ki = mine ? ws.ckey[lane] : ~0ull;
+        int rank = 0;
+        const int tot4 = (total + 3) & ~3;
+#pragma unroll 1
+        for (int j = 0; j < tot4; j += 4) {
+            const ulonglong2 k01 = *reinterpret_cast<const ulonglong2*>(&ws.ckey[j]);
+            const ulonglong2 k23 = *reinterpret_cast<const ulonglong2*>(&ws.ckey[j + 2]);
+            rank += (k01.x < ki) + (k01.y < ki) + (k23.x < ki) + (k23.y < ki);
+        }
+        const u32 hk = (u32)(ki >> 32);
+        const int src = (int)((ki >> 16) & 0xffffu), bin = (int)(ki & 0xffffu);
+        const bool sel = mine && rank < L;
+        if (sel) {
+            ws.sel_src[rank] = src;
+            ws.sel_bin[rank] = bin;
+            ws.sel_w[rank] = ws.wspk(src * C::LPP + FL::owner(bin), FL::slot(bin), FL::twist(src));
+            ws.sel_pm[rank] = key_float(hk);
+        }
+        const int lastl = __ffs(__ballot_sync(kFull, mine && rank == L - 1)) - 1;
+        const u32 hlast = __shfl_sync(kFull, hk, lastl);
+        const u32 lastp = __reduce_or_sync(kFull, sel && hk == hlast ? 1u << src : 0u);
+        exact_needed = __any_sync(kFull, mine && rank >= L && hk == hlast && ((lastp >> src) & 1u));
+        __syncwarp();
+    } else if constexpr (K == L) {
         const u32 pkey = (u32)p << 16;
         auto lane_best = [&](MaskT m, u32& hi, u32& lo) {
             hi = 0xffffffffu;
