@@ -52,22 +52,36 @@ struct SampleArgs {
     signed char sizes[128];
 };
 
-// one record (2MG+2 uint16 = MG+1 words) built in registers, word w handed to put(w, value)
-template <int MN, int MG, typename Put>
-__device__ __forceinline__ void draw_store(uint64_t key, Put&& put) {
-    unsigned cols[MN], icols[MN], b;
-    rmfht_maps::draw_map<MN>(key, cols, icols, b);
-    // record halves: cols of A (MG), b, cols of A^-1 (MG), A^-1 b
-    unsigned h[2 * MG + 2];
+// one record (2MG+2 uint16 = MG+1 words): word w handed to put(w, value),
+// then the columns of A^-1 and A^-1 b as half words put16(half, value) — a
+// basis word's pivot names the column it holds (draw_map_basis), so the
+// columns land at their half-word slots with no register permutation
+template <int MN, int MG, typename Put, typename Put16>
+__device__ __forceinline__ void draw_store(uint64_t key, Put&& put, Put16&& put16) {
+    unsigned cols[MN], ub[MN], pv[MN], b;
+    rmfht_maps::draw_map_basis<MN>(key, cols, ub, pv, b);
+    // record halves: cols of A (MG), b, cols of A^-1 (MG), A^-1 b; whole
+    // words up to half MG, half words after (never both on one location)
+    unsigned h[MG + 2];
 #pragma unroll
-    for (int k = 0; k < MG; k++) {
-        h[k] = k < MN ? cols[k < MN ? k : 0] : 0u;
-        h[MG + 1 + k] = k < MN ? icols[k < MN ? k : 0] : 0u;
-    }
+    for (int k = 0; k < MG + 2; k++) h[k] = 0u;
+#pragma unroll
+    for (int k = 0; k < MN; k++) h[k] = cols[k];
     h[MG] = b;
-    h[2 * MG + 1] = rmfht_maps::inv_shift<MN>(icols, b);
+    constexpr int WF = (MG + 1) / 2;  // words made of halves 0 .. 2 WF - 1 <= MG
 #pragma unroll
-    for (int w = 0; w <= MG; w++) put(w, h[2 * w] | (h[2 * w + 1] << 16));
+    for (int w = 0; w < WF; w++) put(w, h[2 * w] | (h[2 * w + 1] << 16));
+    if constexpr (2 * WF == MG) put16(MG, b);
+#pragma unroll
+    for (int k = MN; k < MG; k++) put16(MG + 1 + k, 0u);
+    unsigned c = 0u;
+#pragma unroll
+    for (int j = 0; j < MN; j++) {
+        const unsigned coef = ub[j] >> 16;
+        put16(MG + 1 + (__ffs(pv[j]) - 1), coef);
+        if (b & pv[j]) c ^= coef;  // A^-1 b = sum over the set bits k of b of column k
+    }
+    put16(2 * MG + 1, c);
 }
 
 // slots below MG-2 variables (r >= 5)
@@ -121,6 +135,10 @@ __global__ void __launch_bounds__(256) sample_kernel(SampleArgs a, uint32_t* rec
                     const unsigned o = o0 + w;
                     stage[o + (o >> 5)] = v;
                 };
+                auto put16 = [&](int hw, unsigned v) {
+                    const unsigned o = o0 + (unsigned)(hw >> 1);
+                    reinterpret_cast<uint16_t*>(stage)[2 * (o + (o >> 5)) + (hw & 1)] = (uint16_t)v;
+                };
                 const int mn = a.sizes[s];
                 if (a.identity_root && at == 0 && s < a.L) {
                     unsigned h[2 * MG + 2];
@@ -132,9 +150,9 @@ __global__ void __launch_bounds__(256) sample_kernel(SampleArgs a, uint32_t* rec
                     continue;
                 }
                 const uint64_t key = rmfht_maps::slot_key(a.seed, f, at, s);
-                if (mn == MG) draw_store<MG, MG>(key, put);
-                else if (mn == MG - 1 && MG > 1) draw_store<(MG > 1 ? MG - 1 : 1), MG>(key, put);
-                else if (mn == MG - 2 && MG > 2) draw_store<(MG > 2 ? MG - 2 : 1), MG>(key, put);
+                if (mn == MG) draw_store<MG, MG>(key, put, put16);
+                else if (mn == MG - 1 && MG > 1) draw_store<(MG > 1 ? MG - 1 : 1), MG>(key, put, put16);
+                else if (mn == MG - 2 && MG > 2) draw_store<(MG > 2 ? MG - 2 : 1), MG>(key, put, put16);
                 else {
                     uint32_t t[W];
                     draw_store_rt<MG>(key, mn, t);

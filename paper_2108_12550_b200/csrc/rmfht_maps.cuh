@@ -124,10 +124,10 @@ struct Word16 {
 // both halves.  After MN columns the u_j are the unit vectors e_{p_j}, so
 // A^-1 e_{p_j} = coef_j: the columns of A^-1 without a Gauss-Jordan pass.
 template <int MN>
-RMFHT_HD void draw_map(uint64_t key, unsigned (&cols)[MN], unsigned (&icols)[MN], unsigned& b) {
+RMFHT_HD void draw_map_basis(uint64_t key, unsigned (&cols)[MN], unsigned (&ub)[MN], unsigned (&pv)[MN], unsigned& b) {
     constexpr unsigned mask = (1u << MN) - 1u;
     Word16 rs(key);
-    unsigned ub[MN], pv[MN];  // basis word (u | coef << 16), pivot bit
+    // ub: basis word (u | coef << 16), pv: its pivot bit
     unsigned pivm = 0u;
 #pragma unroll
     for (int i = 0; i < MN; i++) {
@@ -149,6 +149,14 @@ RMFHT_HD void draw_map(uint64_t key, unsigned (&cols)[MN], unsigned (&icols)[MN]
             if (ub[j] & pv[i]) ub[j] ^= ub[i];
     }
     b = rs.next() & mask;
+}
+
+// After draw_map_basis the basis words are e_{p_j} | coef_j << 16 with
+// A coef_j = e_{p_j}, i.e. column p_j of A^-1 is coef_j
+template <int MN>
+RMFHT_HD void draw_map(uint64_t key, unsigned (&cols)[MN], unsigned (&icols)[MN], unsigned& b) {
+    unsigned ub[MN], pv[MN];
+    draw_map_basis<MN>(key, cols, ub, pv, b);
 #pragma unroll
     for (int k = 0; k < MN; k++) {
         unsigned c = 0u;
