@@ -831,15 +831,26 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
         const u32 B = (u32)(~b) & (u32)(n - 1);
         const u32 Bh = B >> C::LB;
         const int c0 = sgn ^ (__popc(B) & 1) ^ (__popc(B & (u32)u & (u32)(C::LPP - 1)) & 1);
-        constexpr u64 VM = V >= 64 ? ~0ull : ((1ull << V) - 1ull);
-        u64 P = 0;
-        if (Bh & 1u) P ^= 0xAAAAAAAAAAAAAAAAull;
-        if (Bh & 2u) P ^= 0xCCCCCCCCCCCCCCCCull;
-        if (Bh & 4u) P ^= 0xF0F0F0F0F0F0F0F0ull;
-        if (Bh & 8u) P ^= 0xFF00FF00FF00FF00ull;
-        if (Bh & 16u) P ^= 0xFFFF0000FFFF0000ull;
-        if (Bh & 32u) P ^= 0xFFFFFFFF00000000ull;
-        bits = (c0 ? ~P : P) & VM;
+        if constexpr (V <= 32) {  // 32-bit patterns
+            constexpr u32 VM = V >= 32 ? ~0u : ((1u << V) - 1u);
+            u32 P = 0;
+            if (Bh & 1u) P ^= 0xAAAAAAAAu;
+            if (Bh & 2u) P ^= 0xCCCCCCCCu;
+            if (Bh & 4u) P ^= 0xF0F0F0F0u;
+            if (Bh & 8u) P ^= 0xFF00FF00u;
+            if (Bh & 16u) P ^= 0xFFFF0000u;
+            bits = (u64)((c0 ? ~P : P) & VM);
+        } else {
+            constexpr u64 VM = V >= 64 ? ~0ull : ((1ull << V) - 1ull);
+            u64 P = 0;
+            if (Bh & 1u) P ^= 0xAAAAAAAAAAAAAAAAull;
+            if (Bh & 2u) P ^= 0xCCCCCCCCCCCCCCCCull;
+            if (Bh & 4u) P ^= 0xF0F0F0F0F0F0F0F0ull;
+            if (Bh & 8u) P ^= 0xFF00FF00FF00FF00ull;
+            if (Bh & 16u) P ^= 0xFFFF0000FFFF0000ull;
+            if (Bh & 32u) P ^= 0xFFFFFFFF00000000ull;
+            bits = (c0 ? ~P : P) & VM;
+        }
     } else {
         bits = (u64)((__popc((unsigned)(~(b | u)) & (unsigned)(n - 1)) & 1) ^ sgn);
     }
@@ -1120,6 +1131,7 @@ __device__ __forceinline__ float lm_case(const float (&ach)[NS], int delta) {
 template <int NS>
 __device__ __forceinline__ float lm_dispatch(const float (&ach)[NS], int c, int delta) {
     // c is warp-uniform: one indirect branch, no divergence
+    if (c < 1 || c >= NS) __builtin_unreachable();
     switch (c) {
 #define RMFHT_LM_CASE(CC) \
     case CC:              \
