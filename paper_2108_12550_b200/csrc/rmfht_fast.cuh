@@ -42,10 +42,13 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 // f_op (list_engine.py:15-20): min(|a|,|b|) with the sign of a*b
-// (sgn(0) = +1 only changes the sign of a zero result, which never matters)
+// (sgn(0) = +1 only changes the sign of a zero result, which never matters).
+// One FMNMX.XORSIGN: min(|a|,|b|) with sign(a) ^ sign(b) — bit-identical to
+// min(|a|,|b|) | (sign bit of a*b), which it replaces (3 instructions)
 __device__ __forceinline__ float f_op(float a, float b) {
-    const float m = fminf(fabsf(a), fabsf(b));
-    return __int_as_float(__float_as_int(m) | (__float_as_int(a * b) & 0x80000000));
+    float r;
+    asm("min.xorsign.abs.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
 }
 
 constexpr int kCap = 64;  // FHT candidate list capacity (two per lane)

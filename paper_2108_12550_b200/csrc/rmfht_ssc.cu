@@ -28,12 +28,14 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kMaxM = 10;
 
 // f_op, list_engine.py:15-20: min(|a|,|b|) sgn(a) sgn(b).  The sign comes from
-// the product's sign bit (MNMX + MUL + LOP3); it differs from sgn(a)sgn(b)
-// (sgn(0) = +1) only on a zero result, where it yields -0.0 == +0.0 — every
-// downstream use is a comparison with 0 or a sum, so results are unchanged.
+// sign(a) ^ sign(b) (one FMNMX.XORSIGN, the sign bit of a*b); it differs from
+// sgn(a)sgn(b) (sgn(0) = +1) only on a zero result, where it yields
+// -0.0 == +0.0 — every downstream use is a comparison with 0 or a sum, so
+// results are unchanged.
 __device__ __forceinline__ float f_op(float a, float b) {
-    const float m = fminf(fabsf(a), fabsf(b));
-    return __int_as_float(__float_as_int(m) | (__float_as_int(a * b) & 0x80000000));
+    float r;
+    asm("min.xorsign.abs.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
 }
 __device__ __forceinline__ double f_op(double a, double b) {
     const double m = fmin(fabs(a), fabs(b));
