@@ -39,7 +39,7 @@ sys.path.insert(0, ROOT)
 
 # BASELINE.json configurations: name -> (r, m, L, M, permutations, Eb/N0, frames per step)
 CONFIGS = {
-    "rm29_L4_M20": (2, 9, 4, 20, True, 2.5, 16384),   # headline
+    "rm29_L4_M20": (2, 9, 4, 20, True, 2.5, 32768),   # headline
     "rm27_L2_M4": (2, 7, 2, 4, True, 2.0, 262144),
     "rm37_L8_M32": (3, 7, 8, 32, True, 4.0, 16384),
     "rm29_L1_M512": (2, 9, 1, 512, True, 3.0, 1024),
@@ -82,10 +82,13 @@ def _capture(config):
         return {}
 
 
-def _traffic(config):
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture, or None."""
+def _traffic(config, frames):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture
+    (scaled from the captured launch's frame count to this launch's), or None."""
     d = _capture(config)
-    return d["dram_read_bytes"] + d["dram_write_bytes"] if "dram_read_bytes" in d else None
+    if "dram_read_bytes" not in d:
+        return None
+    return (d["dram_read_bytes"] + d["dram_write_bytes"]) * frames / d["frames_per_launch"]
 
 
 def _peaks():
@@ -363,7 +366,7 @@ def run_gpu(args):
             "decode_only": {"value": ws * B * args.steps / (ms_dec / 1e3), "ms_per_step": ms_dec / args.steps,
                             "note": "same batch, permutation table already resident in HBM"},
             "roofline": {"bound": "fp32", "achieved": ach_gops, "peak": peak_gops, "unit": "Gop/s",
-                         "frac": ach_gops / peak_gops, "traffic": _traffic(args.config),
+                         "frac": ach_gops / peak_gops, "traffic": _traffic(args.config, B),
                          "ops_per_frame": ops,
                          "kernel_ms": ms_dec / args.steps,
                          "note": f"reference op ledger per frame x frames per launch / decode-kernel time (CUDA "
