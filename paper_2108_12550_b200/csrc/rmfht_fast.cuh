@@ -974,10 +974,7 @@ __device__ __forceinline__ u64 spc_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
 #pragma unroll
     for (int k = 0; k < V; k++) {
         const int e = LV::full ? k * C::LPP + u : u;
-        if (act) {
-            ws.smag[p * n + e] = fabsf(x[k]);
-            ws.ssgn[p * n + e] = x[k] < 0.f;
-        }
+        if (act) ws.smag[p * n + e] = fabsf(x[k]);
         const u32 bal = __ballot_sync(kFull, act && x[k] < 0.f);
         par ^= __popc(bal & (((1u << (LV::act - 1)) << 1) - 1u) << (p * C::LPP)) & 1;
     }
@@ -995,6 +992,9 @@ __device__ __forceinline__ u64 spc_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
                 rank += (mj < me) || (mj == me && j < e);
             }
             if (rank <= TAU) ws.sord[p * 16 + rank] = (uint16_t)e;
+            // sign bit and the rank (capped at TAU + 1: only ranks 0..TAU are
+            // ever flipped or fixed) for the output bits
+            ws.ssgn[p * n + e] = (uint8_t)((x[k] < 0.f) | ((rank <= TAU ? rank : TAU + 1) << 1));
         }
     }
     __syncwarp();
@@ -1029,16 +1029,19 @@ __device__ __forceinline__ u64 spc_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
                 cand = pmi;
             }
             csrc = i;
-            ws.cpm[lane] = cand;
         }
-        __syncwarp();
+        // stable rank among the 2L candidates (:104), by shuffles
         int rank = 0;
-        if (lane < 2 * L) {
-            for (int c = 0; c < 2 * L; c++) {
-                const float pc = ws.cpm[c];
-                rank += (pc < cand) || (pc == cand && c < lane);
-            }
+#pragma unroll
+        for (int c = 0; c < 2 * L; c++) {
+            const float pc = __shfl_sync(kFull, cand, c);
+            rank += (pc < cand) || (pc == cand && c < lane);
         }
+        // no flip survives and the keeps are already in slot order: the state
+        // is unchanged, and since the later positions are at least as
+        // unreliable (a_{j+1} >= a_j: every flip metric can only grow while
+        // the keeps stay), every later split keeps it too (as spc_node_v1)
+        if (__all_sync(kFull, lane >= 2 * L || ((lane & 1) ? rank >= L : rank == (lane >> 1)))) break;
         // new state (read old state before the sync, write after)
         float npar = 0.f;
         int npa = 0, nfl = 0;
@@ -1061,19 +1064,18 @@ __device__ __forceinline__ u64 spc_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
     // my group's output path is slot p
     const int parent = ws.sel_src[p];
     const int fl = ws.cb[p];
-    int tot = 0;
-    // parity of sign bits of the parent and of the flips
-    for (int j = 0; j < n; j++) tot ^= ws.ssgn[parent * n + j];
-    tot ^= __popc(fl) & 1;
-    const int least = ws.sord[parent * 16];
+    // parity of the parent's sign bits (its ballot parity, sel_bin) and of the flips
+    const int tot = (ws.sel_bin[parent] ^ __popc(fl)) & 1;
     u64 bits = 0;
 #pragma unroll
     for (int k = 0; k < V; k++) {
         const int e = LV::full ? k * C::LPP + u : u;
-        int b = ws.ssgn[parent * n + e];
-        for (int j = 1; j <= TAU; j++)
-            if ((fl >> j & 1) && ws.sord[parent * 16 + j] == e) b ^= 1;
-        if (e == least) b ^= tot;
+        // split j flipped the parent's element of rank j (fl bit j); rank 0
+        // is the least reliable element, which fixes the parity
+        const int sr = act ? ws.ssgn[parent * n + e] : 0;
+        const int r = sr >> 1;
+        int b = (sr & 1) ^ ((fl >> r) & 1);
+        if (r == 0) b ^= tot;
         bits |= (u64)b << k;
     }
     if (lane < L) lin[lane] = (int8_t)ws.sel_src[lane];
