@@ -262,6 +262,30 @@ struct RootIdx {
     __device__ __forceinline__ u32 off(int k) const { return base ^ A[k % NA] ^ B[k / NA]; }
 };
 
+// the same tables for an inner node of size 2^SS: element k*LPP+u maps to
+// index shift ^ cols(e) = base ^ A[k % NA] ^ B[k / NA] (one XOR per element
+// instead of an SS-term GF(2) product)
+template <int SS, int LPP, int V>
+struct NodeIdx {
+    static constexpr int NA = V < 8 ? V : 8;
+    static constexpr int NB = V / NA;
+    u32 base, A[NA], B[NB];
+    __device__ __forceinline__ void build(const uint16_t* cols, u32 shift, int u) {
+        constexpr int LB = clog2(LPP);
+        u32 bse = shift;
+#pragma unroll
+        for (int b = 0; b < LB; b++) bse ^= (u >> b & 1) ? (u32)cols[b] : 0u;
+        base = bse;
+        A[0] = 0;
+#pragma unroll
+        for (int i = 1; i < NA; i++) A[i] = A[i & (i - 1)] ^ (u32)cols[LB + __ffs(i) - 1];
+        B[0] = 0;
+#pragma unroll
+        for (int i = 1; i < NB; i++) B[i] = B[i & (i - 1)] ^ (u32)cols[LB + clog2(NA) + __ffs(i) - 1];
+    }
+    __device__ __forceinline__ u32 at(int k) const { return base ^ A[k % NA] ^ B[k / NA]; }
+};
+
 __device__ __forceinline__ float lds_byte(const float* base, u32 byteoff) {
     return *reinterpret_cast<const float*>(reinterpret_cast<const char*>(base) + byteoff);
 }
@@ -1287,11 +1311,15 @@ __device__ __forceinline__ void perm_ext_inner2(Ctx2<R, MM, L>& cx, float (&x)[L
     const int t = ws.ord[p];
     const int src = t % L;
     const MapR<MM>& mp = cx.maps[base + t];
+    if constexpr (LV::full) {
+        NodeIdx<SS, C::LPP, V> ni;
+        ni.build(mp.icol, (u32)mp.c, u);
+        const float* vs = &ws.vbuf[src * n];
 #pragma unroll
-    for (int k = 0; k < V; k++) {
-        const int e = LV::full ? k * C::LPP + u : u;
-        const u32 j = (u32)mp.c ^ lin_apply<SS>(mp.icol, (u32)e);
-        x[k] = (LV::full || u < n) ? ws.vbuf[src * n + j] : 0.f;
+        for (int k = 0; k < V; k++) x[k] = vs[ni.at(k)];
+    } else {
+        const u32 j = (u32)mp.c ^ lin_apply<SS>(mp.icol, (u32)u);
+        x[0] = u < n ? ws.vbuf[src * n + j] : 0.f;
     }
     float npm = 0.f;
     if (lane < L) npm = ws.pm[ws.ord[lane] % L];
@@ -1417,11 +1445,15 @@ __device__ __forceinline__ u64 node2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / 
             __syncwarp();
             const MapR<MM>& mp = cx.maps[ws.nmap[SS][chain]];
             u64 o2 = 0;
+            if constexpr (LV::full) {
+                NodeIdx<SS, C::LPP, V> ni;
+                ni.build(mp.col, (u32)mp.b, u);
+                const uint8_t* ub = &ws.ubits[p * n];
 #pragma unroll
-            for (int k = 0; k < V; k++) {
-                const int e = LV::full ? k * C::LPP + u : u;
-                const u32 sidx = (u32)mp.b ^ lin_apply<SS>(mp.col, (u32)e);
-                if (LV::full || u < n) o2 |= (u64)ws.ubits[p * n + sidx] << k;
+                for (int k = 0; k < V; k++) o2 |= (u64)ub[ni.at(k)] << k;
+            } else {
+                const u32 sidx = (u32)mp.b ^ lin_apply<SS>(mp.col, (u32)u);
+                if (u < n) o2 = (u64)ws.ubits[p * n + sidx];
             }
             out = o2;
             __syncwarp();
