@@ -667,14 +667,20 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
     const float theta = th0 - (fabsf(th0) + llrabs + fabsf(tau) + fabsf(pmp)) * 9.5367431640625e-07f - 1e-30f;
     using MaskT = typename std::conditional<(V > 32), u64, u32>::type;
     MaskT mask;
+    // LAZY: the spill of the transform (for candidate extraction) is only
+    // needed off the common case; there the lane's single candidate value
+    // (wsel, its last candidate) comes from the mask pass
+    constexpr bool LAZY = sizeof(MaskT) == 4;
+    float wsel = 0.f;
     if constexpr (sizeof(MaskT) == 4) {
-        // one compare and one predicated OR per element
+        // one compare and one predicated OR (and move) per element
         u32 m0 = 0u, m1 = 0u;
 #pragma unroll
         for (int k = 0; k < V; k++) {
             if (fabsf(w[k]) >= theta) {
                 if (k & 1) m1 |= 1u << k;
                 else m0 |= 1u << k;
+                wsel = w[k];
             }
         }
         mask = act ? (m0 | m1) : 0u;
@@ -691,15 +697,18 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
     const int cnt = sizeof(MaskT) == 8 ? __popcll((u64)mask) : __popc((u32)mask);
     const int total = __reduce_add_sync(kFull, cnt);
     // spill the transform for candidate extraction (conflict-free STS.128)
-    if constexpr (V >= 4) {
+    auto spill = [&] {
+        if constexpr (V >= 4) {
 #pragma unroll
-        for (int k = 0; k < V; k += 4)
-            *reinterpret_cast<float4*>(&ws.wspk(lane, k, tw)) = make_float4(w[k], w[k + 1], w[k + 2], w[k + 3]);
-    } else {
+            for (int k = 0; k < V; k += 4)
+                *reinterpret_cast<float4*>(&ws.wspk(lane, k, tw)) = make_float4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+        } else {
 #pragma unroll
-        for (int k = 0; k < V; k++) ws.wspk(lane, k, tw) = w[k];
-    }
-    __syncwarp();
+            for (int k = 0; k < V; k++) ws.wspk(lane, k, tw) = w[k];
+        }
+        __syncwarp();
+    };
+    if constexpr (!LAZY) spill();
     RMFHT_STAT(SS * 8 + 0);
     RMFHT_STAT_ADD(SS * 8 + 4, total);
     // common case: L candidates in all and every path has one (its maximum is
@@ -727,11 +736,12 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
             const int k = (sizeof(MaskT) == 8 ? __ffsll((long long)mask) : __ffs((int)mask)) - 1;
             ws.sel_src[rank] = p;
             ws.sel_bin[rank] = FL::bin(k, u);
-            ws.sel_w[rank] = ws.wspk(lane, k, tw);
+            ws.sel_w[rank] = LAZY ? wsel : ws.wspk(lane, k, tw);
             ws.sel_pm[rank] = cbest;
         }
         __syncwarp();
     } else {
+    if constexpr (LAZY) spill();
     // General case, more than 32 candidates: L rounds of warp-wide minimum
     // selection over the pool key (pm, source path, bin) (:120), each lane
     // offering its best remaining candidate.  The per-path top-K cut (:116, K = L here) can only exclude
