@@ -758,13 +758,19 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
         // (:116, K = L) can only remove a pool top-L candidate through a
         // same-path pm collision at the L-th pick's pm (see the greedy
         // selection below): checked after the ranks.
-        int incl = cnt;
+        int pos;
+        if (__all_sync(kFull, cnt <= 1)) {
+            // at most one candidate per lane: positions from one ballot
+            pos = __popc(__ballot_sync(kFull, cnt > 0) & ((1u << lane) - 1u));
+        } else {
+            int incl = cnt;
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int t = __shfl_up_sync(kFull, incl, off);
-            if (lane >= off) incl += t;
+            for (int off = 1; off < 32; off <<= 1) {
+                const int t = __shfl_up_sync(kFull, incl, off);
+                if (lane >= off) incl += t;
+            }
+            pos = incl - cnt;
         }
-        int pos = incl - cnt;
         MaskT mk = mask;
         while (mk) {
             const int k = (sizeof(MaskT) == 8 ? __ffsll((long long)mk) : __ffs((int)mk)) - 1;
