@@ -187,6 +187,7 @@ struct Ctx2 {
     float ach[C::NS];          // channel layout: ach[s] = alpha[lane + 32 s]
     int lane, p, u;
     u32 alpha_saddr;           // shared-window address of alpha (2 KB aligned)
+    int ngen;                  // RMFHT_STATS only: FHT nodes of this item off the common case
 };
 
 // ------------------------------------------------------------ helpers ----
@@ -710,12 +711,18 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
     };
     if constexpr (!LAZY) spill();
     RMFHT_STAT(SS * 8 + 0);
+#ifdef RMFHT_STATS
+    cx.ngen++;
+#endif
     RMFHT_STAT_ADD(SS * 8 + 4, total);
     // common case: L candidates in all and every path has one (its maximum is
     // always a candidate), i.e. every path's only candidate is its maximum
     const u32 bal = __ballot_sync(kFull, cnt > 0);
     if (total == L && __all_sync(kFull, ((bal >> (p * C::LPP)) & GBITS) != 0u)) {
         RMFHT_STAT(SS * 8 + 1);
+#ifdef RMFHT_STATS
+        cx.ngen--;  // (counted below for every node, undone here)
+#endif
         // the pool is the L path maxima ordered by (pm, source slot) (:116-120)
         int rank = 0;
         if constexpr (C::LPP >= L) {
@@ -1503,10 +1510,25 @@ __device__ __forceinline__ u64 root_node(Ctx2<R, MM, L>& cx, int8_t* lin, F&& al
     int8_t* l2 = ws.l2[MM];
     float xl[VC];
     {
+#ifdef RMFHT_STATS
+        const long long tg = clock64();
+#endif
         RootIdx<MM, C::LPP, LV::V> ri;
         ri.build(ws.comp[p], u, cx.alpha_saddr);
 #pragma unroll
         for (int k = 0; k < VC; k++) xl[k] = f_op(lds_addr(ri.off(k)), lds_addr(ri.off(k + VC)));
+#ifdef RMFHT_STATS
+        {
+            float z = 0.f;
+#pragma unroll
+            for (int k = 0; k < VC; k++) z += xl[k];
+            __syncwarp();
+            const long long dg = clock64() - tg + (z == 1e30f ? 1 : 0);
+            RMFHT_STAT_ADD(244, dg);
+            RMFHT_STAT_ADD(245, dg * dg / 1024);
+            if (lane_id() == 0) atomicMax(&g_stats[246], (unsigned long long)dg);
+        }
+#endif
     }
     const u64 bl = node2<R, MM, L, R - 1, MM - 1, true>(cx, xl, l1);
     float xr[VC];
@@ -1636,6 +1658,7 @@ __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Par
         if (item < items) {
 #ifdef RMFHT_STATS
             const long long t_item = clock64();
+            cx.ngen = 0;
 #endif
             cp_async_wait_all();
             __syncwarp();
@@ -1699,6 +1722,9 @@ __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Par
                 if (lane_id() == 0) atomicMax(&g_stats[203], (unsigned long long)dt);
                 const int bucket = dt < 2048 ? 0 : dt < 65536 ? 1 + (int)((dt - 2048) / 2048) : 33;
                 RMFHT_STAT(210 + bucket);
+                const int ng = cx.ngen < 7 ? cx.ngen : 7;
+                RMFHT_STAT_ADD(150 + ng, dt);
+                RMFHT_STAT(160 + ng);
             }
 #endif
         }

@@ -62,3 +62,10 @@ if cnt:
     print(f"item cycles: mean {mean:.0f}  sd {max(0.0, s2 / cnt - mean * mean) ** 0.5:.0f}  max {mx}")
     hist = st[210:244]
     print("hist (2048-cycle buckets from 2048):", " ".join(str(int(h)) for h in hist))
+    for ng in range(8):
+        c = int(st[160 + ng])
+        if c:
+            print(f"items with {ng} FHT nodes off the common case: {c / cnt:.3f}  mean cycles {int(st[150 + ng]) / c:.0f}")
+    g1, g2, gm = int(st[244]), int(st[245]) * 1024, int(st[246])
+    gmean = g1 / cnt
+    print(f"root f gathers: mean {gmean:.0f} cycles  sd {max(0.0, g2 / cnt - gmean * gmean) ** 0.5:.0f}  max {gm}")
