@@ -1769,24 +1769,26 @@ __global__ void __launch_bounds__(256) reduce_kernel2(rmfht::Params<float> prm, 
         const long long item = f * M + a;
         const AttHdr h = hdr[item];
         if (lane < LPP) sbits[warp][lane] = bitsin[(size_t)item * LPP + lane];
-        if (lane == 0) {
-            MapS im, fm;
+        // the winner's composite sigma = trial o init (columns of A and the
+        // shift), one column per lane: lane k < MM takes column k, lane MM the
+        // shift — A_t (A_i e_k) and A_t b_i ^ b_t
+        if (lane <= MM) {
+            u32 x;
             if (h.init_map < 0) {  // no permutations: identity
-                for (int k = 0; k < rmfht::kMaxM; k++) im.col[k] = im.icol[k] = k < MM ? (1u << k) : 0u;
-                im.b = im.c = 0;
+                x = lane < MM ? (1u << lane) : 0u;
             } else {
-                rmfht::load_map(im, prm.maps + ((size_t)item * S + h.init_map) * REC, MM, MM);
+                x = prm.maps[((size_t)item * S + h.init_map) * REC + lane];  // col[lane] or b (half word MM)
             }
             if (h.trial_map >= 0) {
-                MapS tm;
-                rmfht::load_map(tm, prm.maps + ((size_t)item * S + h.trial_map) * REC, MM, MM);
+                const uint16_t* tr = prm.maps + ((size_t)item * S + h.trial_map) * REC;
+                u32 v = lane == MM ? (u32)tr[MM] : 0u;
 #pragma unroll
-                for (int k = 0; k < MM; k++) fm.col[k] = lin_apply<MM>(tm.col, im.col[k]);
-                fm.b = lin_apply<MM>(tm.col, im.b) ^ tm.b;
-            } else {
-                fm = im;
+                for (int j = 0; j < MM; j++)
+                    if ((x >> j) & 1u) v ^= tr[j];
+                x = v;
             }
-            smap[warp] = fm;
+            if (lane < MM) smap[warp].col[lane] = x;
+            else smap[warp].b = x;
         }
         __syncwarp();
         const MapS& fm = smap[warp];
