@@ -1162,17 +1162,18 @@ __device__ __forceinline__ float multi_tree(float (&v)[T], int lane, int* tri) {
     return v[0];
 }
 
-// LM partial of one lane for pairing direction d (c = d >> 5 != 0): slots
-// with bit hb of s clear, ascending, partner alpha[(l + 32 s) ^ d]
-template <int NS, int CC>
-__device__ __forceinline__ float lm_case(const float (&ach)[NS], int delta) {
-    constexpr int HB = clog2(CC);  // highest set bit of CC
+// c != 0 with highest set bit HB: own slots are the static s with bit HB
+// clear, ascending (the canonical order); the partner alpha[(l ^ delta) + 32 (s ^ c)]
+// comes from the warp's frame copy in shared memory (conflict-free: lane
+// l ^ delta), so only HB selects the code, not c
+template <int NS, int HB>
+__device__ __forceinline__ float lm_hb(const float (&ach)[NS], u32 pc) {
     float acc = 0.f;
     bool first = true;
 #pragma unroll
     for (int s = 0; s < NS; s++) {
         if (s >> HB & 1) continue;
-        const float partner = __shfl_xor_sync(kFull, ach[s ^ CC], delta);
+        const float partner = lds_addr(pc ^ ((u32)s << 7));
         const float m = fminf(fabsf(ach[s]), fabsf(partner));
         acc = first ? m : acc + m;
         first = false;
@@ -1180,30 +1181,26 @@ __device__ __forceinline__ float lm_case(const float (&ach)[NS], int delta) {
     return acc;
 }
 
-template <int NS>
-__device__ __forceinline__ float lm_dispatch(const float (&ach)[NS], int c, int delta) {
-    // c is warp-uniform: one indirect branch, no divergence
-    if (c < 1 || c >= NS) __builtin_unreachable();
-    switch (c) {
-#define RMFHT_LM_CASE(CC) \
-    case CC:              \
-        if constexpr (CC < NS) return lm_case<NS, (CC < NS ? CC : 1)>(ach, delta); \
-        break;
-        RMFHT_LM_CASE(1) RMFHT_LM_CASE(2) RMFHT_LM_CASE(3) RMFHT_LM_CASE(4) RMFHT_LM_CASE(5)
-        RMFHT_LM_CASE(6) RMFHT_LM_CASE(7) RMFHT_LM_CASE(8) RMFHT_LM_CASE(9) RMFHT_LM_CASE(10)
-        RMFHT_LM_CASE(11) RMFHT_LM_CASE(12) RMFHT_LM_CASE(13) RMFHT_LM_CASE(14) RMFHT_LM_CASE(15)
-#undef RMFHT_LM_CASE
-        default:
-            break;
-    }
-    return 0.f;
-}
-
 // LM of trial direction d at the root, canonical channel-domain order
 template <int NS>
-__device__ __forceinline__ float lm_partial_root(const float (&ach)[NS], u32 d, int lane) {
+__device__ __forceinline__ float lm_partial_root(const float (&ach)[NS], u32 d, int lane, u32 alpha_saddr) {
     const int delta = d & 31, c = d >> 5;
-    if (c != 0) return lm_dispatch<NS>(ach, c, delta);
+    if (c != 0) {
+        // partner address with the slot bits of c folded in: (l ^ delta) * 4 + (s ^ c) * 128
+        const u32 pc = (alpha_saddr | ((u32)(lane ^ delta) << 2)) ^ ((u32)c << 7);
+        const int hb = 31 - __clz(c);
+        if (hb < 0 || hb > 3) __builtin_unreachable();
+        if constexpr (NS >= 16) {
+            if (hb == 3) return lm_hb<NS, 3>(ach, pc);
+        }
+        if constexpr (NS >= 8) {
+            if (hb == 2) return lm_hb<NS, (NS >= 8 ? 2 : 0)>(ach, pc);
+        }
+        if constexpr (NS >= 4) {
+            if (hb == 1) return lm_hb<NS, (NS >= 4 ? 1 : 0)>(ach, pc);
+        }
+        return lm_hb<NS, 0>(ach, pc);
+    }
     // d < 32: pairs inside a slot across lanes l, l ^ d; lanes with bit h clear own them
     const int h = 31 - __clz(delta);
     const bool own = !((lane >> h) & 1);
@@ -1246,7 +1243,7 @@ __device__ __forceinline__ void perm_ext_root2(Ctx2<R, MM, L>& cx) {
     }
     __syncwarp();
 #pragma unroll 1
-    for (int t = 0; t < 2 * L; t++) ws.lmp[t][lane] = lm_partial_root<C::NS>(cx.ach, (u32)ws.cb[t], lane);
+    for (int t = 0; t < 2 * L; t++) ws.lmp[t][lane] = lm_partial_root<C::NS>(cx.ach, (u32)ws.cb[t], lane, cx.alpha_saddr);
     __syncwarp();
     float part[2 * L];
 #pragma unroll
