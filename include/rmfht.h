@@ -16,9 +16,14 @@
  * The Python mirror (paper_2108_12550_b200/top_decoders.py) binds these
  * entry points with ctypes; INTEGRATION.md shows the binding.
  *
- * Conventions: all device pointers are caller-owned; launches are ordered on
- * the given cudaStream_t (passed as void*) with no host synchronisation;
- * plans are immutable after creation and may be shared between threads.
+ * Conventions: all device pointers are caller-owned, including the launch
+ * workspace (rmfht_workspace_bytes); launches are ordered on the given
+ * cudaStream_t (passed as void*) with no host synchronisation and no device
+ * allocation; plans hold no device memory and no mutable state after their
+ * one-time kernel setup, so one plan may be launched from several threads
+ * and streams at once (each launch with its own workspace).  Like the
+ * reference functions (pure, top_decoders.py:252-282) a launch reads its
+ * inputs and writes only its outputs and its workspace.
  * Every function returns 0 on success and a negative code on error, with a
  * one-line message from rmfht_last_error() (thread-local).
  */
@@ -99,29 +104,37 @@ int rmfht_sample_maps(const rmfht_plan *plan, uint64_t seed, long long frame0, l
 int rmfht_sample_maps_device(const rmfht_plan *plan, uint64_t seed, long long frame0, long long B,
                              int identity_root, uint16_t *d_rec, void *stream);
 
+/* Bytes of device workspace a launch of B frames needs: the throughput
+ * kernel's per-(frame, attempt) records and, with sampled != 0
+ * (rmfht_decode_launch_sampled), the drawn permutation table.  0 when the
+ * plan's kernel needs none.  Negative on error. */
+long long rmfht_workspace_bytes(const rmfht_plan *plan, long long B, int sampled);
+
 /* Decode B frames whose permutations are drawn on the device from
  * (seed, frame0 + frame index) — no host table ("NULL for
- * on-device sampling with (seed, frame_offset)").  The table lives in a
- * plan-owned device buffer; concurrent calls on one plan must be
- * stream-serialised. */
+ * on-device sampling with (seed, frame_offset)").  The table lives in the
+ * caller's workspace d_work (rmfht_workspace_bytes(plan, B, 1) bytes,
+ * 256-byte aligned); RMFHT_EVALUE if it is missing or too small. */
 int rmfht_decode_launch_sampled(const rmfht_plan *plan, const void *d_llr, uint64_t seed, long long frame0,
                                 int identity_root, uint32_t *d_cw, void *d_pm, int32_t *d_attempt,
-                                int32_t *d_path, long long B, void *stream);
+                                int32_t *d_path, long long B, void *d_work, long long work_bytes, void *stream);
 
 /* Decode B frames.  d_llr [B, 2^m] float or double (per dtype); d_maps
  * [B, M, S, 2m+2] records (ignored without RMFHT_PERMUTATIONS); outputs
  * d_cw [B, max(1, 2^m/32)] bit-packed codewords (bit i%32 of word i/32),
  * d_pm [B] (dtype), d_attempt [B] selected attempt (first strict minimum,
- * top_decoders.py:200), d_path [B] selected path within it (:152). */
+ * top_decoders.py:200), d_path [B] selected path within it (:152).
+ * d_work: rmfht_workspace_bytes(plan, B, 0) bytes (may be NULL when that is 0). */
 int rmfht_decode_launch(const rmfht_plan *plan, const void *d_llr, const uint16_t *d_maps,
                         uint32_t *d_cw, void *d_pm, int32_t *d_attempt, int32_t *d_path,
-                        long long B, void *stream);
+                        long long B, void *d_work, long long work_bytes, void *stream);
 
 /* As above, also writing every attempt's (pm, codeword): d_att_pm [B, M],
  * d_att_cw [B, M, max(1, 2^m/32)] (either may be NULL). */
 int rmfht_decode_launch_diag(const rmfht_plan *plan, const void *d_llr, const uint16_t *d_maps,
                              uint32_t *d_cw, void *d_pm, int32_t *d_attempt, int32_t *d_path,
-                             void *d_att_pm, uint32_t *d_att_cw, long long B, void *stream);
+                             void *d_att_pm, uint32_t *d_att_cw, long long B, void *d_work,
+                             long long work_bytes, void *stream);
 
 /* On-device frames: B frames frame0 .. frame0+B-1 of SNR
  * point `point` — uniform info bits of RM(r, m) (rm_core.py:182-186), polar

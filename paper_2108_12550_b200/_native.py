@@ -30,6 +30,7 @@ EXPORTS = [
     "rmfht_decode_launch", "rmfht_decode_launch_diag", "rmfht_plan_launches_per_call",
     "rmfht_last_error", "rmfht_version", "rmfht_sample_maps", "rmfht_plan_kernel",
     "rmfht_sample_maps_device", "rmfht_decode_launch_sampled", "rmfht_gen_frames", "rmfht_count_errors",
+    "rmfht_workspace_bytes",
 ]
 
 _lib = None
@@ -97,15 +98,17 @@ def lib():
     L.rmfht_plan_kernel.restype = I
     L.rmfht_expand_maps.argtypes = [P, P, P, LL]
     L.rmfht_expand_maps.restype = I
-    L.rmfht_decode_launch.argtypes = [P, P, P, P, P, P, P, LL, P]
+    L.rmfht_workspace_bytes.argtypes = [P, LL, I]
+    L.rmfht_workspace_bytes.restype = LL
+    L.rmfht_decode_launch.argtypes = [P, P, P, P, P, P, P, LL, P, LL, P]
     L.rmfht_decode_launch.restype = I
-    L.rmfht_decode_launch_diag.argtypes = [P, P, P, P, P, P, P, P, P, LL, P]
+    L.rmfht_decode_launch_diag.argtypes = [P, P, P, P, P, P, P, P, P, LL, P, LL, P]
     L.rmfht_decode_launch_diag.restype = I
     L.rmfht_sample_maps.argtypes = [P, ctypes.c_uint64, LL, LL, I, P, P]
     L.rmfht_sample_maps.restype = I
     L.rmfht_sample_maps_device.argtypes = [P, ctypes.c_uint64, LL, LL, I, P, P]
     L.rmfht_sample_maps_device.restype = I
-    L.rmfht_decode_launch_sampled.argtypes = [P, P, ctypes.c_uint64, LL, I, P, P, P, P, LL, P]
+    L.rmfht_decode_launch_sampled.argtypes = [P, P, ctypes.c_uint64, LL, I, P, P, P, P, LL, P, LL, P]
     L.rmfht_decode_launch_sampled.restype = I
     L.rmfht_gen_frames.argtypes = [I, I, ctypes.c_uint64, LL, LL, LL, ctypes.c_double, I, P, P, P]
     L.rmfht_gen_frames.restype = I

@@ -24,7 +24,8 @@ namespace {
 
 template <typename T, int R, int MM, int L>
 int launch_impl(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint32_t* cw, void* pm,
-                int32_t* att, int32_t* path, void* att_pm, uint32_t* att_cw, long long B, cudaStream_t st) {
+                int32_t* att, int32_t* path, void* att_pm, uint32_t* att_cw, long long B, void* /*work: none*/,
+                cudaStream_t st) {
     rmfht::Params<T> prm;
     prm.llr = static_cast<const T*>(llr);
     prm.maps = maps;
@@ -73,7 +74,7 @@ int prepare(rmfht_plan* p) {
 
 template <int R, int MM, int L>
 int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint32_t* cw, void* pm, int32_t* att,
-                int32_t* path, void* att_pm, uint32_t* att_cw, long long B, cudaStream_t st) {
+                int32_t* path, void* att_pm, uint32_t* att_cw, long long B, void* work, cudaStream_t st) {
     rmfht::Params<float> prm;
     prm.llr = static_cast<const float*>(llr);
     prm.maps = maps;
@@ -92,20 +93,11 @@ int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
     std::call_once(mp->once, [mp] { mp->prepared_rc = mp->prepare(mp); });
     if (p->prepared_rc != 0) return p->prepared_rc;
     // the kernel indexes work items with 32-bit integers: at most 2^30 items
-    // (frames x attempts) per launch, larger batches go in frame chunks
-    const long long chunk = p->max_items / p->M > 0 ? p->max_items / p->M : 1;
-    const long long B0 = B < chunk ? B : chunk;
-    const size_t need = (size_t)B0 * p->M * rmfht2::work_bytes2<R, MM, L>();
-    {
-        std::lock_guard<std::mutex> g(mp->work_mu);
-        if (need > mp->work_cap) {
-            if (mp->work) cudaFree(mp->work);
-            mp->work = nullptr;
-            mp->work_cap = 0;
-            if (cudaMalloc(&mp->work, need) != cudaSuccess) return fail(RMFHT_ECUDA, "workspace allocation failed");
-            mp->work_cap = need;
-        }
-    }
+    // (frames x attempts) per launch, larger batches go in frame chunks; the
+    // per-attempt records live in the caller's workspace (sized by
+    // rmfht_workspace_bytes for one chunk), reused chunk after chunk in
+    // stream order
+    const long long chunk = rmfht_chunk_frames(p);
     constexpr int N = 1 << MM, NW = N / 32, S = rmfht::maps_per_attempt(R, MM, L), REC = 2 * MM + 2;
     for (long long f0 = 0; f0 < B; f0 += chunk) {
         const long long Bc = B - f0 < chunk ? B - f0 : chunk;
@@ -120,8 +112,8 @@ int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
         if (prm.att_pm) q.att_pm = prm.att_pm + f0 * p->M;
         if (prm.att_cw) q.att_cw = prm.att_cw + (size_t)f0 * p->M * NW;
         const size_t items = (size_t)Bc * p->M;
-        auto* hdr = static_cast<rmfht2::AttHdr*>(mp->work);
-        auto* bits = reinterpret_cast<unsigned long long*>(static_cast<char*>(mp->work) + items * sizeof(rmfht2::AttHdr));
+        auto* hdr = static_cast<rmfht2::AttHdr*>(work);
+        auto* bits = reinterpret_cast<unsigned long long*>(static_cast<char*>(work) + items * sizeof(rmfht2::AttHdr));
         const long long blocks_needed = ((long long)items + p->nwarps - 1) / p->nwarps;
         const long long grid = blocks_needed < p->grid ? blocks_needed : p->grid;
         if (p->perms) {
@@ -155,10 +147,6 @@ int prepare_fast(rmfht_plan* p) {
     p->nwarps = nw;
     p->smem = smem;
     p->grid = sms * per_sm;
-    if (const char* env = std::getenv("RMFHT_MAX_ITEMS")) {
-        const long long v = std::atoll(env);
-        if (v > 0 && v < p->max_items) p->max_items = v;
-    }
     return 0;
 }
 
@@ -169,6 +157,7 @@ int bind_one(rmfht_plan* p) {
         // the throughput kernel (P == L at every node) does not model: FHT-FSC
         // (L = 1) only
         if (p->fast && (p->perms || L == 1)) {
+            p->work_per_item = rmfht2::work_bytes2<R, MM, L>();
             p->launch = &launch_fast<R, MM, L>;
             p->prepare = &prepare_fast<R, MM, L>;
             return 0;

@@ -3,8 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
-#include <mutex>
 #include <string>
 #include <vector>
 
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(256) sample_kernel(SampleArgs a, uint32_t* rec
 
 extern "C" {
 
-int rmfht_version(void) { return 1; }
+int rmfht_version(void) { return 2; }  // 2: caller-owned workspace (rmfht_workspace_bytes)
 
 const char* rmfht_last_error(void) { return g_err.c_str(); }
 
@@ -217,23 +217,6 @@ int rmfht_plan_create(int r, int m, int L, int M, int flags, int dtype, rmfht_pl
         *out = p;
         return 0;
     }
-    if (flags & RMFHT_AUT_SSC) {
-        // Aut-SSC (top_decoders.py:235-249): P = M SSC decodes, one map of m variables each
-        if (L != 1 || !(flags & RMFHT_PERMUTATIONS)) {
-            delete p;
-            return fail(RMFHT_ECONFIG, "Aut-SSC plans take L = 1 and RMFHT_PERMUTATIONS (P = M decodes)");
-        }
-        p->aut = 1;
-        p->fast = 0;
-        p->sizes.assign(1, m);
-        p->S = 1;
-        if (rmfht_bind_aut_ssc(p) != 0) {
-            delete p;
-            return fail(RMFHT_EUNSUPPORTED, "Aut-SSC supports m <= 10");
-        }
-        *out = p;
-        return 0;
-    }
     if (p->perms) {
         for (int l = 0; l < L; l++) p->sizes.push_back(m);
         if (m - r >= 2)
@@ -241,6 +224,11 @@ int rmfht_plan_create(int r, int m, int L, int M, int flags, int dtype, rmfht_pl
                 for (int t = 0; t < 2 * L; t++) p->sizes.push_back(m - i);
     }
     p->S = (int)p->sizes.size();
+    // tests only: a smaller per-launch item limit exercises the chunked launch path
+    if (const char* env = std::getenv("RMFHT_MAX_ITEMS")) {
+        const long long v = std::atoll(env);
+        if (v > 0 && v < p->max_items) p->max_items = v;
+    }
     const int rc = bind_any(p);
     if (rc != 0) {
         delete p;
@@ -351,43 +339,81 @@ int rmfht_sample_maps_device(const rmfht_plan* p, uint64_t seed, long long frame
     return 0;
 }
 
+// caller-owned workspace: [map table (sampled launches)][per-attempt records of the throughput kernel]
+static size_t table_bytes(const rmfht_plan* p, long long B) {
+    return rmfht_align256((size_t)B * p->M * p->S * (2 * p->m + 2) * sizeof(uint16_t));
+}
+static size_t kernel_work_bytes(const rmfht_plan* p, long long B) {
+    if (!p->work_per_item || B <= 0) return 0;
+    const long long chunk = rmfht_chunk_frames(p);
+    const long long B0 = B < chunk ? B : chunk;
+    return rmfht_align256((size_t)B0 * p->M * p->work_per_item);
+}
+
+long long rmfht_workspace_bytes(const rmfht_plan* p, long long B, int sampled) {
+    if (!p) return fail(RMFHT_EVALUE, "plan is NULL");
+    if (B < 0) return fail(RMFHT_EVALUE, "negative batch");
+    if (B > (1LL << 40) / ((long long)p->M * (p->S + 1))) return fail(RMFHT_EVALUE, "batch too large");
+    size_t t = kernel_work_bytes(p, B);
+    if (sampled && p->perms) t += table_bytes(p, B);
+    return (long long)t;
+}
+
+static int check_work(const rmfht_plan* p, long long B, int sampled, const void* work, long long work_bytes) {
+    const long long need = rmfht_workspace_bytes(p, B, sampled);
+    if (need < 0) return (int)need;
+    if (need > 0 && (!work || work_bytes < need)) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "workspace of %lld bytes required (rmfht_workspace_bytes), %lld given%s", need,
+                 work_bytes, work ? "" : " (NULL)");
+        return fail(RMFHT_EVALUE, buf);
+    }
+    if (need > 0 && (reinterpret_cast<uintptr_t>(work) & 255u)) return fail(RMFHT_EVALUE, "d_work must be 256-byte aligned");
+    return 0;
+}
+
+static int check_io(const rmfht_plan* p, const void* llr, const uint16_t* maps, const uint32_t* cw, const void* pm,
+                    const int32_t* att, const int32_t* path, long long B, int sampled) {
+    if (!p) return fail(RMFHT_EVALUE, "plan is NULL");
+    if (B < 0) return fail(RMFHT_EVALUE, "negative batch");
+    if (B > 0 && (!llr || !cw || !pm || !att || !path || (p->perms && !sampled && !maps)))
+        return fail(RMFHT_EVALUE, "NULL buffer");
+    return 0;
+}
+
 int rmfht_decode_launch_sampled(const rmfht_plan* p, const void* d_llr, uint64_t seed, long long frame0,
                                 int identity_root, uint32_t* d_cw, void* d_pm, int32_t* d_attempt, int32_t* d_path,
-                                long long B, void* stream) {
-    if (!p) return fail(RMFHT_EVALUE, "plan is NULL");
-    if (!p->perms) return rmfht_decode_launch(p, d_llr, nullptr, d_cw, d_pm, d_attempt, d_path, B, stream);
-    auto* mp = const_cast<rmfht_plan*>(p);
-    const size_t need = (size_t)B * p->M * p->S * (2 * p->m + 2) * sizeof(uint16_t);
-    uint16_t* rec;
-    {
-        std::lock_guard<std::mutex> g(mp->work_mu);
-        if (need > mp->maps_cap) {
-            if (mp->maps_buf) cudaFree(mp->maps_buf);
-            mp->maps_buf = nullptr;
-            mp->maps_cap = 0;
-            if (cudaMalloc(&mp->maps_buf, need) != cudaSuccess) return fail(RMFHT_ECUDA, "map table allocation failed");
-            mp->maps_cap = need;
-        }
-        rec = static_cast<uint16_t*>(mp->maps_buf);
-    }
-    int rc = rmfht_sample_maps_device(p, seed, frame0, B, identity_root, rec, stream);
+                                long long B, void* d_work, long long work_bytes, void* stream) {
+    int rc = check_io(p, d_llr, nullptr, d_cw, d_pm, d_attempt, d_path, B, 1);
     if (rc) return rc;
-    return rmfht_decode_launch(p, d_llr, rec, d_cw, d_pm, d_attempt, d_path, B, stream);
+    if ((rc = check_work(p, B, 1, d_work, work_bytes))) return rc;
+    if (B == 0) return 0;
+    if (!p->perms)
+        return p->launch(p, d_llr, nullptr, d_cw, d_pm, d_attempt, d_path, nullptr, nullptr, B, d_work,
+                         static_cast<cudaStream_t>(stream));
+    // the table takes the head of the workspace, the kernel's records the rest
+    uint16_t* rec = static_cast<uint16_t*>(d_work);
+    void* kwork = static_cast<char*>(d_work) + table_bytes(p, B);
+    rc = rmfht_sample_maps_device(p, seed, frame0, B, identity_root, rec, stream);
+    if (rc) return rc;
+    return p->launch(p, d_llr, rec, d_cw, d_pm, d_attempt, d_path, nullptr, nullptr, B, kwork,
+                     static_cast<cudaStream_t>(stream));
 }
 
 int rmfht_decode_launch_diag(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint32_t* cw, void* pm,
-                             int32_t* att, int32_t* path, void* att_pm, uint32_t* att_cw, long long B,
-                             void* stream) {
-    if (!p) return fail(RMFHT_EVALUE, "plan is NULL");
-    if (B < 0) return fail(RMFHT_EVALUE, "negative batch");
-    if (B > 0 && (!llr || !cw || !pm || !att || !path || (p->perms && !maps)))
-        return fail(RMFHT_EVALUE, "NULL buffer");
-    return p->launch(p, llr, maps, cw, pm, att, path, att_pm, att_cw, B, static_cast<cudaStream_t>(stream));
+                             int32_t* att, int32_t* path, void* att_pm, uint32_t* att_cw, long long B, void* d_work,
+                             long long work_bytes, void* stream) {
+    int rc = check_io(p, llr, maps, cw, pm, att, path, B, 0);
+    if (rc) return rc;
+    if ((rc = check_work(p, B, 0, d_work, work_bytes))) return rc;
+    if (B == 0) return 0;
+    return p->launch(p, llr, maps, cw, pm, att, path, att_pm, att_cw, B, d_work, static_cast<cudaStream_t>(stream));
 }
 
 int rmfht_decode_launch(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint32_t* cw, void* pm,
-                        int32_t* att, int32_t* path, long long B, void* stream) {
-    return rmfht_decode_launch_diag(p, llr, maps, cw, pm, att, path, nullptr, nullptr, B, stream);
+                        int32_t* att, int32_t* path, long long B, void* d_work, long long work_bytes, void* stream) {
+    return rmfht_decode_launch_diag(p, llr, maps, cw, pm, att, path, nullptr, nullptr, B, d_work, work_bytes,
+                                    stream);
 }
 
 }  // extern "C"

@@ -1761,7 +1761,8 @@ __global__ void __launch_bounds__(256) reduce_kernel2(rmfht::Params<float> prm, 
         const int oa = __shfl_xor_sync(kFull, ba, off);
         if (oa >= 0 && (ba < 0 || ov < bp || (ov == bp && oa < ba))) { bp = ov; ba = oa; }
     }
-    const int a0 = prm.att_pm ? 0 : ba, a1 = prm.att_pm ? M : ba + 1;
+    const bool diag = prm.att_pm || prm.att_cw;  // either may be NULL (rmfht.h)
+    const int a0 = diag ? 0 : ba, a1 = diag ? M : ba + 1;
     for (int a = a0; a < a1; a++) {
         const long long item = f * M + a;
         const AttHdr h = hdr[item];
@@ -1798,10 +1799,8 @@ __global__ void __launch_bounds__(256) reduce_kernel2(rmfht::Params<float> prm, 
             const u32 word = __ballot_sync(kFull, bit);
             if (lane == t) myword = word;
         }
-        if (prm.att_pm) {
-            if (lane == 0) prm.att_pm[item] = h.pm;
-            if (prm.att_cw && lane < NW) prm.att_cw[item * NW + lane] = myword;
-        }
+        if (prm.att_pm && lane == 0) prm.att_pm[item] = h.pm;
+        if (prm.att_cw && lane < NW) prm.att_cw[item * NW + lane] = myword;
         if (a == ba) {
             if (lane < NW) prm.cw[f * NW + lane] = myword;
             if (lane == 0) {

@@ -10,8 +10,9 @@
 
 #include "../../include/rmfht.h"
 
+// the last pointer is the caller-owned device workspace (rmfht_workspace_bytes)
 using LaunchFn = int (*)(const rmfht_plan*, const void*, const uint16_t*, uint32_t*, void*, int32_t*,
-                         int32_t*, void*, uint32_t*, long long, cudaStream_t);
+                         int32_t*, void*, uint32_t*, long long, void*, cudaStream_t);
 using PrepareFn = int (*)(rmfht_plan*);
 
 struct rmfht_plan {
@@ -27,19 +28,17 @@ struct rmfht_plan {
     std::vector<int> sizes;
     LaunchFn launch;
     PrepareFn prepare;  // CUDA-side binding (shared memory, occupancy), once at the first launch
-    std::once_flag once;
+    std::once_flag once;  // prepare() runs once (function attributes, occupancy); nothing else mutates a plan
     int prepared_rc;
-    // device workspace of the throughput kernel (per-attempt records), grown on demand
-    void* work = nullptr;
-    size_t work_cap = 0;
-    void* maps_buf = nullptr;  // device map table of rmfht_decode_launch_sampled
-    size_t maps_cap = 0;
-    std::mutex work_mu;
-    ~rmfht_plan() {
-        if (work) cudaFree(work);
-        if (maps_buf) cudaFree(maps_buf);
-    }
+    // throughput kernel: per-(frame, attempt) bytes of the caller-owned
+    // workspace (rmfht_workspace_bytes); 0 for kernels that need none
+    size_t work_per_item = 0;
 };
+
+// workspace helpers shared by the C-ABI unit and the binding units
+inline size_t rmfht_align256(size_t x) { return (x + 255) & ~size_t(255); }
+// items the throughput kernel decodes per launch chunk (32-bit item indices)
+inline long long rmfht_chunk_frames(const rmfht_plan* p) { return p->max_items / p->M > 0 ? p->max_items / p->M : 1; }
 
 namespace rmfht_internal {
 int fail(int code, const std::string& msg);

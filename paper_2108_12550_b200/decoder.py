@@ -135,14 +135,46 @@ class Plan:
                                                   rec.data_ptr(), st.cuda_stream))
         return rec
 
-    def launch_sampled(self, llr, seed: int, out: dict, frame0: int = 0, identity_root: bool = True,
-                       stream=None) -> None:
-        """Stream-ordered decode with on-device permutation sampling."""
+    # ------------------------------------------------------- workspace ----
+    def workspace_bytes(self, B: int, sampled: bool = False) -> int:
+        """rmfht_workspace_bytes: device scratch a launch of B frames needs."""
+        n = self._lib.rmfht_workspace_bytes(self._h, B, int(sampled))
+        if n < 0:
+            _check(int(n))
+        return int(n)
+
+    def alloc_workspace(self, B: int, sampled: bool = False, device=None, stream=None):
+        """A caller-owned workspace for launches of up to B frames (None if
+        the plan's kernel needs none).  Allocated on `stream` so torch's
+        caching allocator orders its reuse with that stream."""
+        n = self.workspace_bytes(B, sampled)
+        if n == 0:
+            return None
         torch = _torch()
         st = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(st):
+            return torch.empty(n, dtype=torch.uint8, device=device or torch.device("cuda"))
+
+    def _work(self, B: int, sampled: bool, work, stream):
+        """(tensor kept alive by the caller until the launch is queued, ptr, bytes)"""
+        if work is None:
+            work = self.alloc_workspace(B, sampled, stream=stream)
+        if work is None:
+            return None, None, 0
+        return work, work.data_ptr(), work.numel() * work.element_size()
+
+    def launch_sampled(self, llr, seed: int, out: dict, frame0: int = 0, identity_root: bool = True,
+                       stream=None, work=None) -> None:
+        """Stream-ordered decode with on-device permutation sampling.
+        `work`: a workspace from alloc_workspace(B, sampled=True), else one is
+        allocated for this call."""
+        torch = _torch()
+        st = stream if stream is not None else torch.cuda.current_stream()
+        _keep, wp, wn = self._work(llr.shape[0], True, work, st)
         _check(self._lib.rmfht_decode_launch_sampled(
             self._h, llr.data_ptr(), ctypes.c_uint64(seed), frame0, int(identity_root), out["cw"].data_ptr(),
-            out["pm"].data_ptr(), out["attempt"].data_ptr(), out["path"].data_ptr(), llr.shape[0], st.cuda_stream))
+            out["pm"].data_ptr(), out["attempt"].data_ptr(), out["path"].data_ptr(), llr.shape[0], wp, wn,
+            st.cuda_stream))
 
     # ---------------------------------------------------------- launch ----
     def alloc_outputs(self, B: int, device=None, diag: bool = False):
@@ -160,8 +192,9 @@ class Plan:
             out["att_cw"] = torch.empty((B, self.M, self.words), dtype=torch.int32, device=dev)
         return out
 
-    def launch(self, llr, rec, out: dict, stream=None) -> None:
-        """Stream-ordered launch on device tensors (no host synchronisation)."""
+    def launch(self, llr, rec, out: dict, stream=None, work=None) -> None:
+        """Stream-ordered launch on device tensors (no host synchronisation).
+        `work`: a workspace from alloc_workspace(B), else one is allocated."""
         torch = _torch()
         B = llr.shape[0]
         if llr.shape[-1] != self.N:
@@ -177,14 +210,15 @@ class Plan:
         else:
             rec_ptr = None
         st = stream if stream is not None else torch.cuda.current_stream()
+        _keep, wp, wn = self._work(B, False, work, st)
         diag = "att_pm" in out
         args = [self._h, llr.data_ptr(), rec_ptr, out["cw"].data_ptr(), out["pm"].data_ptr(),
                 out["attempt"].data_ptr(), out["path"].data_ptr()]
         if diag:
             rc = self._lib.rmfht_decode_launch_diag(*args, out["att_pm"].data_ptr(),
-                                                    out["att_cw"].data_ptr(), B, st.cuda_stream)
+                                                    out["att_cw"].data_ptr(), B, wp, wn, st.cuda_stream)
         else:
-            rc = self._lib.rmfht_decode_launch(*args, B, st.cuda_stream)
+            rc = self._lib.rmfht_decode_launch(*args, B, wp, wn, st.cuda_stream)
         _check(rc)
 
     def decode(self, llr, raw_maps=None, records=None, diag: bool = False) -> dict:
@@ -273,6 +307,7 @@ class StreamDecoder:
         self.depth = depth
         self.d_llr = [torch.empty((batch, plan.N), dtype=torch.float32, device=dev) for _ in range(depth)]
         self.out = [plan.alloc_outputs(batch, dev) for _ in range(depth)]
+        self.work = [plan.alloc_workspace(batch, sampled=True, stream=self.compute) for _ in range(depth)]
         self.h_out = [dict(cw=torch.empty((batch, plan.words), dtype=torch.int32).pin_memory(),
                            pm=torch.empty(batch, dtype=torch.float32).pin_memory(),
                            attempt=torch.empty(batch, dtype=torch.int32).pin_memory()) for _ in range(depth)]
@@ -303,7 +338,7 @@ class StreamDecoder:
             self.compute.wait_event(self.out_ready[i])  # previous results of buffer i copied out
             out = {k: v[:n] for k, v in self.out[i].items()}
             self.plan.launch_sampled(self.d_llr[i][:n], self.seed, out, frame0=self.frame0,
-                                     identity_root=self.ident, stream=self.compute)
+                                     identity_root=self.ident, stream=self.compute, work=self.work[i])
             self.done[i].record(self.compute)
         with torch.cuda.stream(self.d2h):
             self.d2h.wait_event(self.done[i])

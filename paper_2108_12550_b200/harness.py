@@ -240,6 +240,7 @@ class DeviceSimulator:
         self.tx = torch.empty((batch, self.dec.plan.words), dtype=torch.int32, device=dev)
         self.out = self.dec.plan.alloc_outputs(batch, dev)
         self.counts = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.work = self.dec.plan.alloc_workspace(batch, sampled=self.dec.perms, device=dev)
 
     def run_batch(self, chan: ChannelConfig, point: int, frame0: int, size: int, table_seed: int,
                   zero_noise: bool = False) -> None:
@@ -249,9 +250,10 @@ class DeviceSimulator:
         out = {k: v[:size] for k, v in self.out.items()}
         gen_frames_device(self.spec, chan, point, frame0, llr, tx, zero_noise)
         if self.dec.perms:
-            self.dec.plan.launch_sampled(llr, table_seed, out, frame0=frame0, identity_root=self.dec.ident)
+            self.dec.plan.launch_sampled(llr, table_seed, out, frame0=frame0, identity_root=self.dec.ident,
+                                         work=self.work)
         else:
-            self.dec.plan.launch(llr, None, out)
+            self.dec.plan.launch(llr, None, out, work=self.work)
         count_errors_device(self.spec, llr, tx, out["cw"], self.counts)
 
     def take_counts(self):

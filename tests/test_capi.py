@@ -86,3 +86,43 @@ def test_uncompiled_shape_binds_generic_kernel():
     rc, h = _create(2, 9, 4, 20, 1, 1)
     assert rc == 0 and lib.rmfht_plan_kernel(h) == 1
     lib.rmfht_plan_destroy(h)
+
+
+def test_workspace_bytes_contract():
+    """Caller-owned workspace (rmfht_workspace_bytes): the throughput kernel
+    needs per-attempt records, sampled launches the table too; the float64
+    kernel needs none; bad batches are ValueError-class."""
+    lib = _native.lib()
+    rc, h = _create(2, 9, 4, 20)
+    w0 = lib.rmfht_workspace_bytes(h, 1000, 0)
+    w1 = lib.rmfht_workspace_bytes(h, 1000, 1)
+    assert 1000 * 20 * (16 + 8 * 8) <= w0 < w1
+    assert w1 - w0 >= 1000 * 20 * 12 * 40
+    assert w0 % 256 == 0 and w1 % 256 == 0
+    assert lib.rmfht_workspace_bytes(h, 0, 1) == 0
+    assert lib.rmfht_workspace_bytes(h, -1, 0) == -2
+    lib.rmfht_plan_destroy(h)
+    rc, h = _create(2, 9, 4, 20, 1, 1)
+    assert lib.rmfht_workspace_bytes(h, 1000, 0) == 0
+    assert lib.rmfht_workspace_bytes(h, 1000, 1) == 1000 * 20 * 12 * 40
+    lib.rmfht_plan_destroy(h)
+
+
+def test_workspace_bytes_contract():
+    """Caller-owned workspace (rmfht_workspace_bytes): the throughput kernel
+    needs per-attempt records, sampled launches the table too; the float64
+    kernel needs none; bad batches are ValueError-class."""
+    lib = _native.lib()
+    rc, h = _create(2, 9, 4, 20)
+    w0 = lib.rmfht_workspace_bytes(h, 1000, 0)
+    w1 = lib.rmfht_workspace_bytes(h, 1000, 1)
+    assert 1000 * 20 * (16 + 8 * 8) <= w0 < w1
+    assert w1 - w0 >= 1000 * 20 * 12 * 40
+    assert w0 % 256 == 0 and w1 % 256 == 0
+    assert lib.rmfht_workspace_bytes(h, 0, 1) == 0
+    assert lib.rmfht_workspace_bytes(h, -1, 0) == -2
+    lib.rmfht_plan_destroy(h)
+    rc, h = _create(2, 9, 4, 20, 1, 1)
+    assert lib.rmfht_workspace_bytes(h, 1000, 0) == 0
+    assert lib.rmfht_workspace_bytes(h, 1000, 1) == 1000 * 20 * 12 * 40
+    lib.rmfht_plan_destroy(h)
