@@ -464,6 +464,27 @@ static int FN(node)(FN(rmo_ctx) *cx, int r, int mn, const REAL *alphas, int p, R
     return q2;
 }
 
+/* The pm the float32 GPU kernels report (rmfht_kernels.cuh, CorrPm): the
+ * decided codeword's metric recomputed from the channel LLRs by the PM
+ * identity 1/2 sum(|a| - (1-2c) a) = sum of |a_i| where (a_i < 0) != c_i,
+ * summed in double in the GPU's order (lane l = i mod 32 adds its positions
+ * in ascending i, then the xor tree 16, 8, 4, 2, 1) and rounded once.  The
+ * float64 mode reports the accumulated metric, as the reference does. */
+static REAL FN(corr_pm)(const REAL *llr, const uint8_t *cw, int N)
+{
+    double q[32], t[32];
+    for (int l = 0; l < 32; l++) {
+        q[l] = 0.0;
+        for (int i = l; i < N; i += 32)
+            if ((llr[i] < 0) != (cw[i] != 0)) q[l] += fabs((double)llr[i]);
+    }
+    for (int off = 16; off >= 1; off >>= 1) {
+        for (int l = 0; l < 32; l++) t[l] = q[l] + q[l ^ off];
+        memcpy(q, t, sizeof q);
+    }
+    return (REAL)q[0];
+}
+
 /* _run_engine, top_decoders.py:116-153 (one attempt). */
 static int FN(attempt)(FN(rmo_ctx) *cx, const REAL *llr, uint8_t *cw, REAL *pm_out, int *path_out)
 {
@@ -552,7 +573,7 @@ int FN(rmo_decode)(int r, int m, int L, int M, int perms, int flags, const REAL 
 #pragma omp for schedule(dynamic, 4)
 #endif
         for (long f = 0; f < B; f++) {
-            REAL best_pm = 0;
+            REAL best_pm = 0, best_rep = 0;
             int best_a = -1, best_path = 0;
             double margin = 1e300;
             uint8_t *bcw = cw_out + (size_t)f * N;
@@ -567,7 +588,10 @@ int FN(rmo_decode)(int r, int m, int L, int M, int perms, int flags, const REAL 
                 int rc = FN(attempt)(&cx, llr + (size_t)f * N, cw, &pm, &path);
                 if (rc != 0) { err = rc; continue; }
                 if (cx.margin < margin) margin = cx.margin;
-                if (att_pm) att_pm[(size_t)f * M + a] = pm;
+                /* reported pm: accumulated (float64 = the reference) or the
+                 * float32 kernels' recomputed metric; selection stays on pm */
+                const REAL rep = sizeof(REAL) == 4 ? FN(corr_pm)(llr + (size_t)f * N, cw, N) : pm;
+                if (att_pm) att_pm[(size_t)f * M + a] = rep;
                 if (att_cw) memcpy(att_cw + ((size_t)f * M + a) * N, cw, (size_t)N);
                 if (best_a >= 0) {
                     int differ = memcmp(bcw, cw, (size_t)N) != 0;
@@ -577,11 +601,11 @@ int FN(rmo_decode)(int r, int m, int L, int M, int perms, int flags, const REAL 
                     }
                 }
                 if (best_a < 0 || pm < best_pm) {          /* :200 strict < */
-                    best_pm = pm; best_a = a; best_path = path;
+                    best_pm = pm; best_rep = rep; best_a = a; best_path = path;
                     memcpy(bcw, cw, (size_t)N);
                 }
             }
-            pm_out[f] = best_pm;
+            pm_out[f] = best_rep;
             if (attempt_out) attempt_out[f] = best_a;
             if (path_out) path_out[f] = best_path;
             if (margin_out) margin_out[f] = margin;

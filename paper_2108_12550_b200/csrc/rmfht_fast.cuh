@@ -1791,20 +1791,26 @@ __global__ void __launch_bounds__(256) reduce_kernel2(rmfht::Params<float> prm, 
         __syncwarp();
         const MapS& fm = smap[warp];
         u32 myword = 0;
+        // reported pm: the decided codeword's metric from the channel LLRs
+        // (rmfht::CorrPm); the accumulated h.pm selected the attempt
+        rmfht::CorrPm corr;
+        const float* fl = prm.llr + (size_t)f * N;
 #pragma unroll
         for (int t = 0; t < NW; t++) {
             const u32 i = (u32)(t * 32 + lane);
             const u32 e = fm.b ^ lin_apply<MM>(fm.col, i);
             const int bit = (int)((sbits[warp][e % LPP] >> (e / LPP)) & 1ull);
+            corr.add(__ldg(fl + i), bit);
             const u32 word = __ballot_sync(kFull, bit);
             if (lane == t) myword = word;
         }
-        if (prm.att_pm && lane == 0) prm.att_pm[item] = h.pm;
+        const float rep = corr.total();
+        if (prm.att_pm && lane == 0) prm.att_pm[item] = rep;
         if (prm.att_cw && lane < NW) prm.att_cw[item * NW + lane] = myword;
         if (a == ba) {
             if (lane < NW) prm.cw[f * NW + lane] = myword;
             if (lane == 0) {
-                prm.pm[f] = h.pm;
+                prm.pm[f] = rep;
                 prm.attempt[f] = ba;
                 prm.path[f] = h.path;
             }

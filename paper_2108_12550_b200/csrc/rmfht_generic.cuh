@@ -35,6 +35,7 @@ struct Small {
     int16_t nmap[kMaxDepth][kMaxL];
     int8_t ident[kMaxL], rootlin[kMaxL], rootchain[kMaxL];
     T best_pm;
+    T best_rep;  // reported pm of the best attempt (rmfht::CorrPm for float32)
     int best_att, best_path, next_map, spc_cnt;
     uint32_t best_cw[32];
 };
@@ -603,22 +604,27 @@ __global__ void __launch_bounds__(128) decode_kernel_generic(rmfht::Params<T> pr
             const int mi = (root_internal && prm.perms) ? sm.rootchain[best] : sm.rootlin[best];
             const MapS& mp = w.comp[mi];
             uint32_t myword = 0;
+            rmfht::CorrPm corr;
             for (int t = 0; t < NW; t++) {
                 const int i = t * 32 + lane;
                 int bit = 0;
                 if (i < N) {
                     const uint32_t src = prm.perms ? fwd_rt(mp, MM, (uint32_t)i) : (uint32_t)i;
                     bit = w.rootout[best * N + src];
+                    if constexpr (sizeof(T) == 4) corr.add((float)alpha[i], bit);
                 }
                 const uint32_t word = __ballot_sync(kFull, bit);
                 if (lane == t) myword = word;
             }
-            if (prm.att_pm && lane == 0) prm.att_pm[(size_t)f * prm.M + a] = pm;
+            T rep = pm;
+            if constexpr (sizeof(T) == 4) rep = (T)corr.total();
+            if (prm.att_pm && lane == 0) prm.att_pm[(size_t)f * prm.M + a] = rep;
             if (prm.att_cw && lane < NW) prm.att_cw[((size_t)f * prm.M + a) * NW + lane] = myword;
             if (!have || pm < sm.best_pm) {
                 if (lane < NW) sm.best_cw[lane] = myword;
                 if (lane == 0) {
                     sm.best_pm = pm;
+                    sm.best_rep = rep;
                     sm.best_att = a;
                     sm.best_path = best;
                 }
@@ -641,7 +647,7 @@ __global__ void __launch_bounds__(128) decode_kernel_generic(rmfht::Params<T> pr
             const Small<T>& o = *reinterpret_cast<Small<T>*>(wbase + (size_t)bw * lay.total + lay.small);
             if (lane < NW) prm.cw[f * NW + lane] = o.best_cw[lane];
             if (lane == 0) {
-                prm.pm[f] = o.best_pm;
+                prm.pm[f] = o.best_rep;
                 prm.attempt[f] = o.best_att;
                 prm.path[f] = o.best_path;
             }

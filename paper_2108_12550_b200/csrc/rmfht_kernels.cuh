@@ -79,6 +79,30 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 template <typename T>
 __device__ __forceinline__ T tabs(T x) { return x < T(0) ? -x : x; }
 
+// Reported path metric of the float32 kernels: the metric of the decided
+// codeword recomputed from the channel LLRs by the PM identity (SURVEY
+// §8(a): PM = 1/2 sum(|a| - (1-2c) a) = the sum of |a_i| over the positions
+// whose hard decision disagrees with c) — the "ML-in-list by correlation" of
+// the north star.  The accumulated float32 metric (fht_decode.py:119, ...)
+// selects paths and attempts as the reference does; but its node increments
+// 1/2 (llr_abs - |w|) cancel catastrophically in float32, so it is only
+// reported to ~1e-4 absolute.  This sum has no cancellation: each lane adds
+// its positions i = 32 t + lane in ascending t in double, then a xor tree
+// (16, 8, 4, 2, 1); rounded once.  The oracle's float32 mode restates it
+// (rmo_impl.h, corr_pm).
+struct CorrPm {
+    double acc = 0.0;
+    __device__ __forceinline__ void add(float a, int bit) {
+        if ((a < 0.f) != (bit != 0)) acc += fabs((double)a);
+    }
+    __device__ __forceinline__ float total() {
+        double v = acc;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) v = v + __shfl_xor_sync(kFull, v, off);
+        return (float)v;
+    }
+};
+
 // offsets of level s in the per-level buffers
 template <typename T, int R, int MM, int L>
 __device__ __forceinline__ int lvl_off(int s) { return L * ((1 << s) - 1); }
@@ -98,6 +122,7 @@ struct alignas(16) WarpWS {
     T lm[2 * L];
     T cpm[L * L], cabs[L * L], cw[L * L];
     T best_pm;
+    T best_rep;  // reported pm of the best attempt (CorrPm for float32)
     MapS maps[S > 0 ? S : 1];
     MapS comp[L];                    // root paths: composite of init and root trial maps
     MapS tcomp[2 * L];
@@ -650,6 +675,7 @@ __global__ void __launch_bounds__(256) decode_kernel(Params<T> prm) {
             const int mi = ROOT_INTERNAL ? ws.rootchain[best] : ws.rootlin[best];
             const MapS& mp = ws.comp[mi];
             uint32_t myword = 0;
+            CorrPm corr;
 #pragma unroll
             for (int t = 0; t < NW; t++) {
                 const int i = t * 32 + lane;
@@ -657,15 +683,18 @@ __global__ void __launch_bounds__(256) decode_kernel(Params<T> prm) {
                 if (i < N) {
                     const uint32_t src = prm.perms ? map_fwd<MM>(mp, (uint32_t)i) : (uint32_t)i;
                     bit = ws.rootout[best * N + src];
+                    if constexpr (sizeof(T) == 4) corr.add((float)alpha[i], bit);
                 }
                 const uint32_t word = __ballot_sync(kFull, bit);
                 if (lane == t) myword = word;
             }
-            if (prm.att_pm && lane == 0) prm.att_pm[(size_t)f * prm.M + a] = pm;
+            T rep = pm;
+            if constexpr (sizeof(T) == 4) rep = (T)corr.total();
+            if (prm.att_pm && lane == 0) prm.att_pm[(size_t)f * prm.M + a] = rep;
             if (prm.att_cw && lane < NW) prm.att_cw[((size_t)f * prm.M + a) * NW + lane] = myword;
             if (!have || pm < ws.best_pm) {  // strict <, earlier attempt keeps ties (:200)
                 if (lane < NW) ws.best_cw[lane] = myword;
-                if (lane == 0) { ws.best_pm = pm; ws.best_att = a; ws.best_path = best; }
+                if (lane == 0) { ws.best_pm = pm; ws.best_rep = rep; ws.best_att = a; ws.best_path = best; }
                 have = true;
             }
             __syncwarp();
@@ -687,7 +716,7 @@ __global__ void __launch_bounds__(256) decode_kernel(Params<T> prm) {
             const WS& o = wsarr[bw];
             if (lane < NW) prm.cw[f * NW + lane] = o.best_cw[lane];
             if (lane == 0) {
-                prm.pm[f] = o.best_pm;
+                prm.pm[f] = o.best_rep;
                 prm.attempt[f] = o.best_att;
                 prm.path[f] = o.best_path;
             }
