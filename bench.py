@@ -2,23 +2,37 @@
 
 Workload (BASELINE.json headline): RM(2,9), M=20 affine automorphisms
 (decoder 0's root maps = identity), L=4, BPSK/AWGN float32 LLRs at
-Eb/N0 = 2.5 dB.  One step = one decode launch over a batch of frames whose
-LLRs and permutation tables are resident in HBM (together larger than the
-126 MB L2, so no flush is needed between steps).
+Eb/N0 = 2.5 dB.  One step = one pass of the hot path over a batch of
+frames resident in HBM (larger than the 126 MB L2, so no flush is needed
+between steps): on-device permutation sampling + decode + per-frame pick.
 
   value     decoded frames/s of the whole job (sum over ranks / max time)
-  e2e       same metric through the public C-ABI path with host buffers:
-            pinned host LLRs + map records copied in, codewords/PM/attempt
-            copied out, every step
+  e2e       same metric through the public API with host buffers
+            (decoder.StreamDecoder -> rmfht_decode_launch_sampled): pinned
+            host LLRs copied in and codewords / PM / attempt copied out
+            every step; permutations are drawn on the device, so no table
+            crosses the host link
   roofline  reference op ledger (accounting.complexity_model, include_perm)
             per frame x frames/s against the FP32 issue peak
             (SMs x 128 lanes x max SM clock); HBM bound alongside
-  cpu_baseline  the CPU oracle port (float64 restatement of the reference)
-            on this host's cores, bounded sample
+  cpu_baseline  the float64 C port of the reference (oracle/) on this host's
+            cores over a bounded sample: the first frames of the GPU's own
+            batch under the same permutation table, so the same sample also
+            yields ``ties`` — the tie accounting of the GPU's answers against
+            the port (oracle/ties.py)
+  cpu_baseline_reference  the UNMODIFIED Python reference
+            (baseline/_ref: rmworkbench.harness._simulate_chunk, its stock
+            per-frame path) on all host cores, bounded sample
+
+--gpus N without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU, frames sharded, seeds
+distinct per rank, no data-path collective).  --dry-run runs the same
+launch/timing plumbing on CPU ranks (gloo) with a stand-in step (tests).
 
 --impl reference times the CPU restatement of the reference decoder (the
-reference is pure Python with no native path; the oracle port is its CPU
-implementation here) on the same config, rank 0 only.
+reference is pure Python with no native path; the float64 C port is its CPU
+implementation here) on the same config, rank 0 only, and reports the
+unmodified Python reference beside it.
 """
 
 from __future__ import annotations
@@ -55,8 +69,12 @@ WORKLOAD = "RM(2,9) p-FHT-FSCL L=4 M=20 (decoder 0 = identity), Eb/N0 2.5 dB"
 METRIC = "decoded frames/s, RM(2,9) M=20 L=4, 1 B200; % of roofline; vs host CPU"
 
 
+CURRENT = "rm29_L4_M20"
+
+
 def select_config(name):
-    global R, M_VARS, L, M, PERMS, AUT, EBN0, WORKLOAD
+    global R, M_VARS, L, M, PERMS, AUT, EBN0, WORKLOAD, CURRENT
+    CURRENT = name
     r, m, l, mm, perms, ebn0, frames = CONFIGS[name]
     AUT = perms == "aut"
     R, M_VARS, L, M, PERMS, EBN0 = r, m, l, mm, bool(perms), ebn0
@@ -150,6 +168,18 @@ def _dist():
     return ws, rank, local
 
 
+def _relaunch(args):
+    """--gpus N outside torchrun: re-exec under torch.distributed.run with N
+    ranks on 127.0.0.1 (the driver's own launch line)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def make_inputs(plan, spec, B, seed):
     """Frames and permutation records for one batch (host)."""
     from paper_2108_12550_b200.channel_model import synthetic_frames
@@ -178,36 +208,110 @@ def _cpu_batches(B, count, seed0):
     return out
 
 
-def _cpu_decode(llr, raw, cores):
+def _cpu_decode(llr, raw, cores, want_attempts=False):
     from oracle import oracle
     if AUT:
-        oracle.aut_ssc(R, M_VARS, M, llr, raw[:, :, 0, :], dtype=np.float64, nthreads=cores)
-        return
-    oracle.decode(R, M_VARS, L, M if PERMS else 1, llr, raw, perms=PERMS, dtype=np.float64, nthreads=cores,
-                  want_attempts=False)
+        return oracle.aut_ssc(R, M_VARS, M, llr, raw[:, :, 0, :], dtype=np.float64, nthreads=cores)
+    return oracle.decode(R, M_VARS, L, M if PERMS else 1, llr.astype(np.float64), raw, perms=PERMS,
+                         dtype=np.float64, nthreads=cores, want_attempts=want_attempts)
 
 
-def cpu_baseline(seconds: float = 12.0):
-    """Oracle port (float64 restatement) on all host cores over a bounded sample."""
+def cpu_baseline(plan, llr, x, gpu, seed, seconds: float = 12.0):
+    """The float64 C port (oracle/) on all host cores over a bounded sample:
+    the first frames of the GPU's batch with the same permutation table
+    (plan.sample(seed) = the table the device drew), so the same decodes give
+    the tie accounting of the GPU's answers against the port (oracle/ties.py).
+    Returns (cpu_baseline, ties)."""
+    from oracle import ties as T
     cores = os.cpu_count() or 1
-    done, t_used, frames = 0, 0.0, 0
-    B = 16 * cores
-    # calibrate the batch so one call is ~1/8 of the budget
-    (llr, raw), = _cpu_batches(B, 1, 1000)
-    t0 = time.perf_counter()
-    _cpu_decode(llr, raw, cores)
-    dt = time.perf_counter() - t0
-    B = max(B, int(B * (seconds / 8) / max(dt, 1e-3)))
-    while t_used < seconds and done < 64:
-        (llr, raw), = _cpu_batches(B, 1, 1001 + done)
+    B = llr.shape[0]
+    cmax = max(16, (1 << 26) // max(1, M * (1 << M_VARS)))  # bounds the per-attempt outputs of a chunk
+    C = min(cmax, 4 * cores)  # the first chunk calibrates the rest to ~1/6 of the budget each
+    frames, t_used, parts, c0 = 0, 0.0, [], 0
+    while c0 < B and t_used < seconds:
+        c1 = min(B, c0 + C)
+        raw = None
+        if PERMS:
+            raw, _ = plan.sample(c1 - c0, seed, frame0=c0, identity_root=not AUT, want_records=False)
         t0 = time.perf_counter()
-        _cpu_decode(llr, raw, cores)
+        p = _cpu_decode(llr[c0:c1], raw, cores, want_attempts=not AUT)
         t_used += time.perf_counter() - t0
-        frames += B
-        done += 1
-    return {"value": frames / t_used, "unit": "frames/s", "cores": cores, "kind": "port",
-            "sample": f"{frames} frames of the workload ({done} batches of {B}), float64 oracle port, "
-                      f"{cores} threads, {t_used:.1f} s"}
+        if not AUT:
+            parts.append(T.classify(gpu["cw"][c0:c1], gpu["pm"][c0:c1], gpu["attempt"][c0:c1], p, x=x[c0:c1]))
+        frames += c1 - c0
+        c0 = c1
+        C = max(16, min(cmax, int(frames * (seconds / 6) / max(t_used, 1e-6))))
+    base = {"value": frames / t_used, "unit": "frames/s", "cores": cores, "kind": "port",
+            "sample": f"frames 0..{frames - 1} of the GPU's batch under the same permutation table, float64 "
+                      f"C port of the reference (oracle/), {cores} threads, {t_used:.1f} s"}
+    tie = None
+    if parts:
+        tie = T.merge(parts)
+        tie["ok"] = T.ok(tie)
+        tie["note"] = ("GPU float32 vs float64 port on the same float32 LLRs and table (oracle/ties.py): "
+                       "codeword mismatches must sit on frames with a selection margin <= rel, attempt "
+                       "mismatches must be pm-equivalent (same codeword, pm within rel) or on such frames; "
+                       "ens_exact_ties = frames whose minimum pm is reached by >= 2 attempts")
+    return base, tie
+
+
+def _ref_cfg():
+    from rmworkbench.top_decoders import DecoderConfig
+    if AUT:
+        return DecoderConfig("Aut-SSC", P=M)
+    if not PERMS:
+        return DecoderConfig("FHT-FSC" if L == 1 else "FHT-FSCL", L=L)
+    return DecoderConfig("p-FHT-FSCL", L=L, M=M)
+
+
+def _ref_chunk(a):
+    sys.path.insert(0, a[0])
+    from rmworkbench import rm_core
+    from rmworkbench.channel_model import ChannelConfig
+    from rmworkbench.harness import SimJob, _simulate_chunk
+    job = SimJob(r=R, m=M_VARS, decoder=_ref_cfg(), ebn0_points=(EBN0,), max_frames=a[2], seed=777)
+    spec = rm_core.build_code(R, M_VARS)
+    chan = ChannelConfig.for_rate(EBN0, spec.rate, 777)
+    t0 = time.perf_counter()
+    err, ml = _simulate_chunk(job, spec, chan, 0, a[1], a[2])
+    return err, ml, time.perf_counter() - t0
+
+
+def cpu_baseline_reference(seconds: float = 12.0):
+    """The UNMODIFIED Python reference (baseline/_ref, installed from
+    /root/reference) on all host cores: its stock per-frame harness path
+    rmworkbench.harness._simulate_chunk (frame generation, decode, error
+    count; harness.py:94-113) over a bounded sample, one chunk per core."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "rmworkbench")):
+        return {"unavailable": "baseline/_ref is not installed (pip install --target baseline/_ref, DESIGN.md)"}
+    from concurrent.futures import ProcessPoolExecutor
+    cores = os.cpu_count() or 1
+    try:
+        e, ml, dt = _ref_chunk((ref, 0, 1))  # calibration: one frame in-process (also warms the imports)
+    except Exception as ex:  # noqa: BLE001
+        return {"unavailable": f"reference import failed: {ex!r}"}
+    per = max(1, int(seconds / max(dt, 1e-4)))
+    t0 = time.perf_counter()
+    with ProcessPoolExecutor(max_workers=cores, initializer=_select_in_worker, initargs=(CURRENT,)) as ex:
+        res = list(ex.map(_ref_chunk, [(ref, 1 + c * per, per) for c in range(cores)]))
+    wall = time.perf_counter() - t0
+    frames = per * cores
+    cpu = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            cpu = next(l.split(":", 1)[1].strip() for l in fh if l.startswith("model name"))
+    except Exception:  # noqa: BLE001
+        pass
+    return {"value": frames / wall, "unit": "frames/s", "cores": cores, "kind": "reference", "cpu": cpu,
+            "sample": f"{frames} frames ({cores} processes x {per}) of the reference harness stream "
+                      f"frame_rng(777, 0, k) through the unmodified Python reference "
+                      f"(baseline/_ref rmworkbench.harness._simulate_chunk), wall {wall:.1f} s incl. process "
+                      f"start; frame errors {sum(r[0] for r in res)}"}
+
+
+def _select_in_worker(name):
+    select_config(name)
 
 
 def run_reference(args):
@@ -237,6 +341,8 @@ def run_reference(args):
                              "sample": f"{B} frames per step x {args.steps} steps, float64 CPU restatement "
                                        f"of the reference decoder (oracle/), {cores} threads"},
             "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if not args.no_cpu:
+        line["reference_python"] = cpu_baseline_reference(args.cpu_seconds)
     print(json.dumps(line), flush=True)
 
 
@@ -246,8 +352,12 @@ def run_gpu(args):
 
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
+    comm = 1
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = dist.get_world_size()
+        if rank == 0:
+            print(f"bench: NCCL communicator of {comm} ranks", file=sys.stderr, flush=True)
     from paper_2108_12550_b200.decoder import Plan
     from paper_2108_12550_b200.plan import complexity_ops
     from paper_2108_12550_b200.rm_core import build_code
@@ -300,6 +410,10 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     value = ws * B * args.steps / (ms / 1e3)
+    # the timed steps' answers (every step decodes the same batch and table)
+    gpu_host = {"cw": np.unpackbits(out["cw"].cpu().numpy().view(np.uint32).view(np.uint8), axis=-1,
+                                    bitorder="little")[:, :spec.N],
+                "pm": out["pm"].cpu().numpy(), "attempt": out["attempt"].cpu().numpy()}
 
     # decode only, permutation table resident in HBM (explains value)
     for _ in range(2):
@@ -360,6 +474,7 @@ def run_gpu(args):
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "nccl_world": comm,
             "config": {"workload": WORKLOAD, "frames_per_step": B, "parallelism": f"replicas{ws}",
                        "l2": f"inputs {(llr.nbytes + (recs.nbytes if recs is not None else 0)) / 2**20:.0f} MiB/step > 126 MB L2, no flush",
                        "fer_check": fer_warm},
@@ -390,8 +505,53 @@ def run_gpu(args):
                                       "unit": "G warp-inst/s", "frac": ipf * kern_fps / 1e9 / peak_i,
                                       "inst_per_frame": ipf}
         if not args.no_cpu and ws == 1:
-            line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+            base, tie = cpu_baseline(plan, llr, x, gpu_host, SEED, args.cpu_seconds)
+            line["cpu_baseline"] = base
+            if tie is not None:
+                line["ties"] = tie
+            line["cpu_baseline_reference"] = cpu_baseline_reference(args.cpu_seconds)
         print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def run_dry(args):
+    """The launch / timing / reduction plumbing on CPU ranks (gloo), with a
+    stand-in step (hard decisions of the rank's own frames, no decoder):
+    rank count, per-rank seeds, barrier + max-over-ranks time, rank-summed
+    frames.  Tests only."""
+    import torch
+    import torch.distributed as dist
+    from paper_2108_12550_b200.channel_model import synthetic_frames
+    from paper_2108_12550_b200.rm_core import build_code
+    ws, rank, _ = _dist()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    _, llr = synthetic_frames(build_code(R, M_VARS), EBN0, args.frames, seed=1 + rank)
+    for _ in range(args.warmup):
+        np.signbit(llr).sum()
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    done = 0
+    for _ in range(args.steps):
+        done += int(np.signbit(llr).any(axis=1).shape[0])
+    if ws > 1:
+        dist.barrier()
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    n = torch.tensor([done], dtype=torch.int64)
+    firsts = [None] * ws
+    if ws > 1:
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        dist.all_reduce(n, op=dist.ReduceOp.SUM)
+        dist.all_gather_object(firsts, float(llr[0, 0]))
+    else:
+        firsts = [float(llr[0, 0])]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "n_gpus": ws, "steps": args.steps,
+                          "warmup": args.warmup, "frames_total": int(n[0]), "value": int(n[0]) / float(dt),
+                          "unit": "frames/s", "rank_first_llr": firsts,
+                          "config": {"workload": WORKLOAD, "frames_per_step": args.frames}}), flush=True)
     if ws > 1:
         dist.destroy_process_group()
 
@@ -409,13 +569,22 @@ def main():
     ap.add_argument("--no-lockstep", action="store_true", help="throughput kernel without per-round barriers")
     ap.add_argument("--lockstep", type=int, default=16, choices=[4, 8, 16], help="warps per lock-step group")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--dry-run", action="store_true", help="CPU ranks (gloo), stand-in step: plumbing tests only")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        _relaunch(args)  # does not return
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}: launch one rank per GPU "
+                 f"(torchrun --nproc-per-node {args.gpus}) or omit WORLD_SIZE to let bench.py spawn them")
     if args.warmup < 3:
         args.warmup = 3
     frames = select_config(args.config)
     if args.frames is None:
         args.frames = frames
-    if args.impl == "reference":
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_gpu(args)
