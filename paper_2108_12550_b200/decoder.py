@@ -16,12 +16,12 @@ import numpy as np
 
 from . import _native
 from .automorphism import random_raw_table
-from .rm_core import ConfigurationError, build_code
+from .rm_core import ConfigurationError, UnsupportedShape, build_code
 
 _ERRS = {
     _native.RMFHT_ECONFIG: ConfigurationError,
     _native.RMFHT_EVALUE: ValueError,
-    _native.RMFHT_EUNSUPPORTED: ConfigurationError,
+    _native.RMFHT_EUNSUPPORTED: UnsupportedShape,
 }
 
 

@@ -360,6 +360,61 @@ def records_to_json(records) -> str:
     return json.dumps([asdict(r) for r in records], indent=1)
 
 
+def emit(records, path: str, fmt: str = "csv") -> None:
+    """harness.py:220-229: write the records as CSV or JSON."""
+    if fmt == "csv":
+        text = records_to_csv(records)
+    elif fmt == "json":
+        text = records_to_json(records)
+    else:
+        raise ConfigurationError(f"unknown output format {fmt!r}")
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write(text)
+
+
+def job_from_dict(cfg: dict) -> SimJob:
+    """harness.py:248-262: a SimJob from the reference's job-file schema
+    ({"code": [r, m], "decoder": {"algorithm", "L", "M", "P",
+    "permutations_enabled"}, "ebn0_points", "max_frames",
+    "min_frame_errors", "seed", "workers", "zero_noise"}), plus the optional
+    GPU batch size "batch"."""
+    dec = cfg["decoder"]
+    decoder = DecoderConfig(algorithm=dec["algorithm"], L=int(dec.get("L", 1)), M=int(dec.get("M", 1)),
+                            P=int(dec.get("P", 1)),
+                            permutations_enabled=bool(dec.get("permutations_enabled", True)),
+                            seed=int(cfg.get("seed", 0)))
+    code = cfg["code"]
+    extra = {"batch": int(cfg["batch"])} if "batch" in cfg else {}
+    return SimJob(r=int(code[0]), m=int(code[1]), decoder=decoder, ebn0_points=tuple(cfg["ebn0_points"]),
+                  max_frames=int(cfg.get("max_frames", 10000)),
+                  min_frame_errors=int(cfg.get("min_frame_errors", 100)), seed=int(cfg.get("seed", 0)),
+                  workers=int(cfg.get("workers", 1)), zero_noise=bool(cfg.get("zero_noise", False)), **extra)
+
+
+def simulate(config_path: str, out: str | None = None, fmt: str = "csv", seed: int | None = None,
+             workers: int | None = None, zero_noise: bool = False, rank: int = 0, world: int = 1,
+             group=None) -> str:
+    """The drop-in for ``rmwb simulate --config job.json`` (cli.py:46-63):
+    read the reference-format job file, apply the same overrides, run the
+    job on the GPU (run_job) and either write the records to ``out``
+    (``emit``) or return them as CSV / JSON text.  ``workers`` is accepted
+    and recorded for schema parity; the GPU decodes in batches instead."""
+    with open(config_path, "r", encoding="utf-8") as fh:
+        cfg = json.load(fh)
+    if seed is not None:
+        cfg["seed"] = seed
+    if workers is not None:
+        cfg["workers"] = workers
+    if zero_noise:
+        cfg["zero_noise"] = True
+    records = run_job(job_from_dict(cfg), rank=rank, world=world, group=group)
+    if out:
+        if rank == 0:
+            emit(records, out, fmt)
+        return ""
+    return records_to_csv(records) if fmt == "csv" else records_to_json(records)
+
+
 def parse_csv(text: str) -> list:
     out = []
     for row in csv.DictReader(io.StringIO(text)):

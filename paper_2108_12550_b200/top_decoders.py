@@ -17,7 +17,7 @@ import numpy as np
 from .automorphism import maps_to_raw, sample_affine, sample_affine_batch
 from .decoder import get_plan
 from .plan import map_sizes, plan_visits
-from .rm_core import CodeSpec, ConfigurationError
+from .rm_core import CodeSpec, ConfigurationError, UnsupportedShape  # noqa: F401 (re-exported)
 
 ALGORITHMS = ("SC", "SCL", "FSCL", "FHT-FSC", "FHT-FSCL", "p-FHT-FSCL",
               "Aut-SSC", "RPA", "SRPA")

@@ -126,3 +126,17 @@ def test_workspace_bytes_contract():
     assert lib.rmfht_workspace_bytes(h, 1000, 0) == 0
     assert lib.rmfht_workspace_bytes(h, 1000, 1) == 1000 * 20 * 12 * 40
     lib.rmfht_plan_destroy(h)
+
+
+def test_unsupported_shape_is_a_configuration_error():
+    """RMFHT_EUNSUPPORTED surfaces as top_decoders.UnsupportedShape, a
+    ConfigurationError subclass the INTEGRATION.md binding falls back on."""
+    from paper_2108_12550_b200.decoder import Plan
+    from paper_2108_12550_b200.rm_core import ConfigurationError
+    from paper_2108_12550_b200.top_decoders import UnsupportedShape
+    assert issubclass(UnsupportedShape, ConfigurationError)
+    with pytest.raises(UnsupportedShape):
+        Plan(2, 12, 4, 5)
+    with pytest.raises(ConfigurationError) as e:
+        Plan(2, 15, 4, 5)
+    assert not isinstance(e.value, UnsupportedShape)

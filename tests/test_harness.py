@@ -132,3 +132,48 @@ def test_two_ranks_gloo_equal_one_rank():
     for p in procs:
         p.join(timeout=60)
     assert got[0] == one and got[1] == one
+
+
+# ------------------------------------------------ job files and persistence
+# the reference's documented job file (pkg/README.md "Command line"), the
+# golden_fer.csv acceptance run
+JOB_JSON = {"code": [2, 6], "decoder": {"algorithm": "p-FHT-FSCL", "L": 4}, "ebn0_points": [2.0, 2.5],
+            "max_frames": 30000, "min_frame_errors": 1000000000, "seed": 777, "workers": 2}
+
+
+def test_job_from_dict_reference_schema():
+    """harness.py:248-262 field by field."""
+    job = harness.job_from_dict(JOB_JSON)
+    assert (job.r, job.m) == (2, 6)
+    assert job.decoder == DecoderConfig("p-FHT-FSCL", L=4, M=1, P=1, permutations_enabled=True, seed=777)
+    assert job.ebn0_points == (2.0, 2.5) and job.max_frames == 30000
+    assert job.min_frame_errors == 10 ** 9 and job.seed == 777 and job.workers == 2 and not job.zero_noise
+    j2 = harness.job_from_dict({"code": [2, 9], "decoder": {"algorithm": "p-FHT-FSCL", "L": 4, "M": 20,
+                                                             "permutations_enabled": False},
+                                "ebn0_points": [3.0], "batch": 4096})
+    assert j2.decoder.M == 20 and not j2.decoder.permutations_enabled and j2.batch == 4096
+    assert j2.max_frames == 10000 and j2.min_frame_errors == 100 and j2.seed == 0
+    with pytest.raises(ConfigurationError):
+        harness.job_from_dict({"code": [2, 9], "decoder": {"algorithm": "p-FHT-FSCL", "L": 0},
+                               "ebn0_points": [3.0]})
+    with pytest.raises(ConfigurationError):
+        harness.job_from_dict({"code": [2, 9], "decoder": {"algorithm": "p-FHT-FSCL"}, "ebn0_points": [3.0, 2.0]})
+
+
+def test_emit_csv_json_roundtrip(tmp_path):
+    """harness.py:198-229: emit writes what records_to_csv / _json return;
+    the CSV parses back to the same records; unknown formats raise."""
+    recs = [harness.FerRecord(r=2, m=6, decoder="p-FHT-FSCL", L=4, M=1, P=1, ebn0_db=2.0, frames=30000,
+                              frame_errors=748, fer=748 / 30000, ml_lb_fer=629 / 30000, avg_additions=1252.0,
+                              avg_comparisons=832.0, time_steps=46, mem_bits=11008, wall_seconds=0.25, seed=777)]
+    p = tmp_path / "r.csv"
+    harness.emit(recs, str(p), "csv")
+    text = p.read_text()
+    assert text == harness.records_to_csv(recs)
+    assert text.splitlines()[0] == ",".join(harness.CSV_HEADER)
+    assert harness.parse_csv(text) == recs
+    q = tmp_path / "r.json"
+    harness.emit(recs, str(q), "json")
+    assert json.loads(q.read_text())[0]["frame_errors"] == 748
+    with pytest.raises(ConfigurationError):
+        harness.emit(recs, str(tmp_path / "r.txt"), "xml")

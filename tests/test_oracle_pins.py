@@ -7,10 +7,12 @@ field bit-for-bit; the float32 restatement must match exactly on
 exact-arithmetic fixtures and stay within the fp32 tolerance on channel
 fixtures.
 """
+import os
+
 import numpy as np
 import pytest
 
-from conftest import aut_names, golden_names, load_aut, load_golden
+from conftest import GOLDEN, aut_names, golden_names, load_aut, load_golden
 
 NAMES = golden_names()
 AUT = aut_names()
@@ -81,3 +83,23 @@ def test_aut_ssc_f32_oracle(oracle_mod, name):
         picked = sc[np.arange(len(sc)), o["winner"]]
         assert np.all(picked >= g["score"] - 1e-5 * np.abs(g["score"]) - 1e-4)
         assert np.mean(o["winner"] == g["winner"]) > 0.9
+
+
+def test_golden_fer_rows_pinned_by_port():
+    """The reference's own golden FER file (pkg/data/golden_fer.csv:1-5,
+    copied to tests/golden/ref_golden_fer.csv by tools/copy_ref_golden.sh):
+    the float64 port on the reference harness stream (tools/fer_port.py,
+    tests/golden/fer_points.json "golden_*") reproduces frames, frame errors
+    and the ML bound of every row exactly — FHT-FSCL needs no table, and
+    p-FHT-FSCL (M = 1) the frame generator's own draws, replayed."""
+    import csv
+    import json
+    pts = json.load(open(os.path.join(GOLDEN, "fer_points.json")))
+    rows = list(csv.DictReader(open(os.path.join(GOLDEN, "ref_golden_fer.csv"))))
+    assert len(rows) == 4
+    for row in rows:
+        name = "golden_rm26_fhtfscl_L4" if row["decoder"] == "FHT-FSCL" else "golden_rm26_pfhtfscl_L4"
+        pt = next(p for p in pts[name]["points"] if p["ebn0"] == float(row["ebn0_db"]))
+        assert pt["frames"] == int(row["frames"])
+        assert pt["errors"] == int(row["frame_errors"]), (name, row)
+        assert pt["ml_errors"] == round(float(row["ml_lb_fer"]) * int(row["frames"])), (name, row)
