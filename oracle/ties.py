@@ -25,7 +25,10 @@ the same permutation table:
   when the port's own pm for the GPU's attempt is within ``rel`` of its
   minimum and that attempt's codeword equals the port's answer (the same
   decision reached by another attempt), else ``_other``; ``_unexcused``
-  counts the ones that are neither pm-equivalent nor on a near-tie frame.
+  counts the ones that are neither pm-equivalent nor on a near-tie frame;
+  ``_on_exact_ties`` the ones where the GPU picked another attempt of the
+  port's exactly tied minimum (same codeword, bit-identical float64 pm): the
+  "exact path-metric ties" of the north star.
 * ``pm_max_rel``: max |pm_gpu - pm_port| / max(|pm_port|, 1).
 """
 
@@ -62,6 +65,8 @@ def classify(gpu_cw, gpu_pm, gpu_att, port, rel: float = REL, x=None) -> dict:
     else:
         same_cw = np.ones(B, dtype=bool)
     att_equiv = att_diff & pm_equiv & same_cw
+    # the GPU's attempt is one of the port's exactly tied minimum attempts
+    on_exact = att_diff & (att_pm[idx, ga] == ppm) & same_cw
     pm_rel = np.abs(gpu_pm.astype(np.float64) - ppm) / scale
     out = dict(
         frames=int(B),
@@ -70,6 +75,7 @@ def classify(gpu_cw, gpu_pm, gpu_att, port, rel: float = REL, x=None) -> dict:
         cw_mismatch=int(cw_diff.sum()), cw_mismatch_excused=int((cw_diff & tie_frame).sum()),
         cw_mismatch_unexcused=int((cw_diff & ~tie_frame).sum()),
         attempt_mismatch=int(att_diff.sum()), attempt_mismatch_pm_equivalent=int(att_equiv.sum()),
+        attempt_mismatch_on_exact_ties=int(on_exact.sum()),
         attempt_mismatch_unexcused=int((att_diff & ~att_equiv & ~tie_frame).sum()),
         pm_max_rel=float(pm_rel.max()) if B else 0.0,
         pm_over_tol=int((pm_rel > rel).sum()),
