@@ -24,8 +24,8 @@ namespace {
 
 template <typename T, int R, int MM, int L>
 int launch_impl(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint32_t* cw, void* pm,
-                int32_t* att, int32_t* path, void* att_pm, uint32_t* att_cw, long long B,
-                const rmfht_sample_spec* /*table in maps*/, void* /*work: none*/, cudaStream_t st) {
+                int32_t* att, int32_t* path, void* att_pm, uint32_t* att_cw, long long B, void* /*work: none*/,
+                cudaStream_t st) {
     rmfht::Params<T> prm;
     prm.llr = static_cast<const T*>(llr);
     prm.maps = maps;
@@ -74,8 +74,7 @@ int prepare(rmfht_plan* p) {
 
 template <int R, int MM, int L>
 int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint32_t* cw, void* pm, int32_t* att,
-                int32_t* path, void* att_pm, uint32_t* att_cw, long long B, const rmfht_sample_spec* samp, void* work,
-                cudaStream_t st) {
+                int32_t* path, void* att_pm, uint32_t* att_cw, long long B, void* work, cudaStream_t st) {
     rmfht::Params<float> prm;
     prm.llr = static_cast<const float*>(llr);
     prm.maps = maps;
@@ -89,13 +88,6 @@ int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
     prm.path = path;
     prm.att_pm = static_cast<float*>(att_pm);
     prm.att_cw = att_cw;
-    if (samp) {
-        prm.maps = nullptr;
-        prm.sampled = 1;
-        prm.seed = samp->seed;
-        prm.frame0 = samp->frame0;
-        prm.identity_root = samp->identity_root;
-    }
     if (B <= 0) return 0;
     auto* mp = const_cast<rmfht_plan*>(p);
     std::call_once(mp->once, [mp] { mp->prepared_rc = mp->prepare(mp); });
@@ -113,7 +105,6 @@ int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
         q.B = Bc;
         q.llr = prm.llr + f0 * N;
         if (prm.maps) q.maps = prm.maps + (size_t)f0 * p->M * S * REC;
-        q.frame0 = prm.frame0 + f0;
         q.cw = prm.cw + f0 * NW;
         q.pm = prm.pm + f0;
         q.attempt = prm.attempt + f0;
@@ -125,11 +116,10 @@ int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
         auto* bits = reinterpret_cast<unsigned long long*>(static_cast<char*>(work) + items * sizeof(rmfht2::AttHdr));
         const long long blocks_needed = ((long long)items + p->nwarps - 1) / p->nwarps;
         const long long grid = blocks_needed < p->grid ? blocks_needed : p->grid;
-        const int threads = (p->nwarps + 1) * 32;  // + the record-producer warp
         if (p->perms) {
-            rmfht2::decode_kernel2<R, MM, L, true><<<(unsigned)grid, threads, p->smem, st>>>(q, hdr, bits);
+            rmfht2::decode_kernel2<R, MM, L, true><<<(unsigned)grid, p->nwarps * 32, p->smem, st>>>(q, hdr, bits);
         } else if constexpr (L == 1) {
-            rmfht2::decode_kernel2<R, MM, L, false><<<(unsigned)grid, threads, p->smem, st>>>(q, hdr, bits);
+            rmfht2::decode_kernel2<R, MM, L, false><<<(unsigned)grid, p->nwarps * 32, p->smem, st>>>(q, hdr, bits);
         }
         rmfht2::reduce_kernel2<R, MM, L><<<(unsigned)((Bc + 7) / 8), 256, 0, st>>>(q, hdr, bits);
     }
@@ -140,7 +130,8 @@ int launch_fast(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
 
 template <int R, int MM, int L>
 int prepare_fast(rmfht_plan* p) {
-    const int nw = rmfht2::fast_warps<R, MM, L>();  // fits 227 KB (the sm_100 opt-in maximum) by construction
+    int nw = rmfht2::fast_warps<R, MM, L>();
+    while (nw > 4 && rmfht2::smem_bytes2<R, MM, L>(nw) > 227 * 1024) nw -= 4;  // 227 KB: the sm_100 opt-in maximum
     const size_t smem = rmfht2::smem_bytes2<R, MM, L>(nw);
     auto kern = rmfht2::decode_kernel2<R, MM, L, true>;
     if constexpr (L == 1) {
@@ -151,7 +142,7 @@ int prepare_fast(rmfht_plan* p) {
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (nw + 1) * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem);
     if (e != cudaSuccess || per_sm < 1) return fail(RMFHT_ECUDA, "kernel does not fit an SM");
     p->nwarps = nw;
     p->smem = smem;
@@ -167,7 +158,6 @@ int bind_one(rmfht_plan* p) {
         // (L = 1) only
         if (p->fast && (p->perms || L == 1)) {
             p->work_per_item = rmfht2::work_bytes2<R, MM, L>();
-            p->fused_sampling = 1;
             p->launch = &launch_fast<R, MM, L>;
             p->prepare = &prepare_fast<R, MM, L>;
             return 0;

@@ -43,8 +43,6 @@ int bind_any(rmfht_plan* p) {
     return fail(RMFHT_EUNSUPPORTED, buf);
 }
 
-using rmfht_maps::draw_store;
-using rmfht_maps::draw_store_rt;
 using rmfht_maps::expand_one;
 
 struct SampleArgs {
@@ -53,6 +51,54 @@ struct SampleArgs {
     int M, S, L, m, identity_root;
     signed char sizes[128];
 };
+
+// one record (2MG+2 uint16 = MG+1 words): word w handed to put(w, value),
+// then the columns of A^-1 and A^-1 b as half words put16(half, value) — a
+// basis word's pivot names the column it holds (draw_map_basis), so the
+// columns land at their half-word slots with no register permutation
+template <int MN, int MG, typename Put, typename Put16>
+__device__ __forceinline__ void draw_store(uint64_t key, Put&& put, Put16&& put16) {
+    unsigned cols[MN], ub[MN], pv[MN], b;
+    rmfht_maps::draw_map_basis<MN>(key, cols, ub, pv, b);
+    // record halves: cols of A (MG), b, cols of A^-1 (MG), A^-1 b; whole
+    // words up to half MG, half words after (never both on one location)
+    unsigned h[MG + 2];
+#pragma unroll
+    for (int k = 0; k < MG + 2; k++) h[k] = 0u;
+#pragma unroll
+    for (int k = 0; k < MN; k++) h[k] = cols[k];
+    h[MG] = b;
+    constexpr int WF = (MG + 1) / 2;  // words made of halves 0 .. 2 WF - 1 <= MG
+#pragma unroll
+    for (int w = 0; w < WF; w++) put(w, h[2 * w] | (h[2 * w + 1] << 16));
+    if constexpr (2 * WF == MG) put16(MG, b);
+#pragma unroll
+    for (int k = MN; k < MG; k++) put16(MG + 1 + k, 0u);
+    unsigned c = 0u;
+#pragma unroll
+    for (int j = 0; j < MN; j++) {
+        const unsigned coef = ub[j] >> 16;
+        put16(MG + 1 + (__ffs(pv[j]) - 1), coef);
+        if (b & pv[j]) c ^= coef;  // A^-1 b = sum over the set bits k of b of column k
+    }
+    put16(2 * MG + 1, c);
+}
+
+// slots below MG-2 variables (r >= 5)
+template <int MG>
+__device__ __noinline__ void draw_store_rt(uint64_t key, int mn, uint32_t* o) {
+    unsigned cols[16], icols[16], b;
+    rmfht_maps::draw_map_rt(key, mn, cols, icols, b);
+    unsigned cinv = 0, h[2 * MG + 2];
+    for (int k = 0; k < MG; k++) {
+        h[k] = k < mn ? cols[k] : 0u;
+        h[MG + 1 + k] = k < mn ? icols[k] : 0u;
+        if (k < mn && ((b >> k) & 1u)) cinv ^= icols[k];
+    }
+    h[MG] = b;
+    h[2 * MG + 1] = cinv;
+    for (int w = 0; w <= MG; w++) o[w] = h[2 * w] | (h[2 * w + 1] << 16);
+}
 
 // A CTA draws the records of G consecutive (frame, attempt) items: warp w
 // takes slots w, w + 8, ... with one lane per item (a warp's lanes draw maps
@@ -204,7 +250,7 @@ int rmfht_plan_map_sizes(const rmfht_plan* p, int* sizes) {
 
 int rmfht_plan_record_u16(const rmfht_plan* p) { return p ? 2 * p->m + 2 : fail(RMFHT_EVALUE, "plan is NULL"); }
 
-int rmfht_plan_launches_per_call(const rmfht_plan* p) { return p ? (p->fast ? 2 : 1) : 0; }  // + 1 when sampled without fused sampling
+int rmfht_plan_launches_per_call(const rmfht_plan* p) { return p ? (p->fast ? 2 : 1) : 0; }  // + 1 when sampled
 
 int rmfht_plan_kernel(const rmfht_plan* p) { return p ? (p->aut ? 4 : p->fast ? 2 : (p->generic ? 3 : 1)) : 0; }
 
@@ -309,7 +355,7 @@ long long rmfht_workspace_bytes(const rmfht_plan* p, long long B, int sampled) {
     if (B < 0) return fail(RMFHT_EVALUE, "negative batch");
     if (B > (1LL << 40) / ((long long)p->M * (p->S + 1))) return fail(RMFHT_EVALUE, "batch too large");
     size_t t = kernel_work_bytes(p, B);
-    if (sampled && p->perms && !p->fused_sampling) t += table_bytes(p, B);
+    if (sampled && p->perms) t += table_bytes(p, B);
     return (long long)t;
 }
 
@@ -343,20 +389,14 @@ int rmfht_decode_launch_sampled(const rmfht_plan* p, const void* d_llr, uint64_t
     if ((rc = check_work(p, B, 1, d_work, work_bytes))) return rc;
     if (B == 0) return 0;
     if (!p->perms)
-        return p->launch(p, d_llr, nullptr, d_cw, d_pm, d_attempt, d_path, nullptr, nullptr, B, nullptr, d_work,
+        return p->launch(p, d_llr, nullptr, d_cw, d_pm, d_attempt, d_path, nullptr, nullptr, B, d_work,
                          static_cast<cudaStream_t>(stream));
-    if (p->fused_sampling) {
-        // the throughput kernel draws its own records (producer warp)
-        const rmfht_sample_spec spec{seed, frame0, identity_root};
-        return p->launch(p, d_llr, nullptr, d_cw, d_pm, d_attempt, d_path, nullptr, nullptr, B, &spec, d_work,
-                         static_cast<cudaStream_t>(stream));
-    }
     // the table takes the head of the workspace, the kernel's records the rest
     uint16_t* rec = static_cast<uint16_t*>(d_work);
     void* kwork = static_cast<char*>(d_work) + table_bytes(p, B);
     rc = rmfht_sample_maps_device(p, seed, frame0, B, identity_root, rec, stream);
     if (rc) return rc;
-    return p->launch(p, d_llr, rec, d_cw, d_pm, d_attempt, d_path, nullptr, nullptr, B, nullptr, kwork,
+    return p->launch(p, d_llr, rec, d_cw, d_pm, d_attempt, d_path, nullptr, nullptr, B, kwork,
                      static_cast<cudaStream_t>(stream));
 }
 
@@ -367,8 +407,7 @@ int rmfht_decode_launch_diag(const rmfht_plan* p, const void* llr, const uint16_
     if (rc) return rc;
     if ((rc = check_work(p, B, 0, d_work, work_bytes))) return rc;
     if (B == 0) return 0;
-    return p->launch(p, llr, maps, cw, pm, att, path, att_pm, att_cw, B, nullptr, d_work,
-                     static_cast<cudaStream_t>(stream));
+    return p->launch(p, llr, maps, cw, pm, att, path, att_pm, att_cw, B, d_work, static_cast<cudaStream_t>(stream));
 }
 
 int rmfht_decode_launch(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint32_t* cw, void* pm,

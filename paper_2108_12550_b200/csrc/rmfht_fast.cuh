@@ -27,7 +27,6 @@
 #include <type_traits>
 
 #include "rmfht_kernels.cuh"  // MapS, Params, maps_per_attempt, helpers
-#include "rmfht_maps.cuh"     // slot_key, draw_store (the record-producer warp)
 
 namespace rmfht2 {
 
@@ -1564,17 +1563,11 @@ __device__ __forceinline__ u64 root_node(Ctx2<R, MM, L>& cx, int8_t* lin, F&& al
     return out;
 }
 
-// per-attempt record written by decode_kernel2, reduced by reduce_kernel2:
-// the best path's pm and slot, and its forward composite root map
-// sigma = trial o init (columns fwd[0..m-1], shift fwd[m]) — the reduce
-// kernel un-permutes the winner with it (top_decoders.py:147-150), so it
-// needs no map table
+// per-attempt record written by decode_kernel2, reduced by reduce_kernel2
 struct AttHdr {
     float pm;
-    int path;
-    uint16_t fwd[12];
+    int path, init_map, trial_map;
 };
-static_assert(sizeof(AttHdr) == 32, "AttHdr layout");
 
 template <int R, int MM, int L>
 __host__ __device__ constexpr size_t smem_bytes2(int nwarps) {
@@ -1582,154 +1575,71 @@ __host__ __device__ constexpr size_t smem_bytes2(int nwarps) {
     return 2048 + size_t(1 << MM) * 4 * size_t(nwarps) + sizeof(WS2<R, MM, L>) * size_t(nwarps);
 }
 
-// decoding warps per CTA: 31 (with the record-producer warp 32, i.e. a
-// 64-register cap), else 4 fewer at a time (27, 23: 80 registers) until the
-// LLR copies and scratch fit in 227 KB of shared memory
+// warps per CTA: the largest multiple of 4 (at most 32, i.e. a 64-register
+// cap) whose LLR copies and scratch fit in 227 KB of shared memory
 template <int R, int MM, int L>
 __host__ __device__ constexpr int fast_warps() {
 #ifdef RMFHT_FAST_WARPS_MAX
     int w = RMFHT_FAST_WARPS_MAX;  // A/B builds only (tools/build_variant.py)
 #else
-    int w = 31;  // + the record-producer warp: a multiple of 4 warps in all (one register file quarter per SMSP)
+    int w = 32;
 #endif
-    while (w > 3 && smem_bytes2<R, MM, L>(w) > 227 * 1024) w -= 4;  // 31, 27, 23, ...
+    while (w > 4 && smem_bytes2<R, MM, L>(w) > 227 * 1024) w -= 4;
     return w;
 }
 
 // ------------------------------------------------------------- kernel ----
-// Record-producer warp (warp 0 of the CTA): writes the map records of every
-// decoding warp's NEXT work item into that warp's idle record buffer while
-// the current round decodes, and the round barrier publishes them.  With
-// on-device tables (prm.sampled) it draws them (slot_key / draw_store, the
-// same code as rmfht_sample_maps: bit-identical tables, no table in HBM);
-// with a table it copies the item's records from global memory.
-template <int R, int MM, int L, bool PM>
-__device__ __forceinline__ void produce_round(const rmfht::Params<float>& prm, WS2<R, MM, L>* wsarr, int base,
-                                              int buf, int items, int lane) {
-    using C = Cfg<R, MM, L>;
-    constexpr int S = C::S, W = MM + 1;  // records per item, 32-bit words per record
-    constexpr int nwarps = fast_warps<R, MM, L>();
-    if constexpr (PM && S > 0) {
-        if (prm.sampled) {
-            const unsigned M = (unsigned)prm.M;
-#pragma unroll 1
-            for (int t = lane; t < nwarps * S; t += 32) {
-                const int w = t / S, s = t - (t / S) * S;
-                const int item = base + w;
-                if (item >= items) continue;
-                const unsigned q = (unsigned)item / M;
-                const int at = (int)((unsigned)item - q * M);
-                uint32_t* dst = reinterpret_cast<uint32_t*>(wsarr[w].recs[buf]) + s * W;
-                auto put = [&](int k, unsigned v) { dst[k] = v; };
-                auto put16 = [&](int h, unsigned v) { reinterpret_cast<uint16_t*>(dst)[h] = (uint16_t)v; };
-                // slot sizes (rmfht_plan_create): L root maps of m variables,
-                // then 2L per permutation node i of m - i variables
-                const int mn = s < L ? MM : MM - (s - L) / (2 * L);
-                if (prm.identity_root && at == 0 && s < L) {
-#pragma unroll
-                    for (int k = 0; k < W; k++) {
-                        const unsigned lo = (2 * k < MM) ? 1u << (2 * k) : 0u;
-                        const unsigned hi = (2 * k + 1 < MM) ? 1u << (2 * k + 1) : 0u;
-                        dst[k] = lo | (hi << 16);  // columns of A; b = 0 at half MM
-                    }
-#pragma unroll
-                    for (int k = 0; k < MM; k++) put16(MM + 1 + k, 1u << k);  // columns of A^-1
-                    put16(2 * MM + 1, 0u);
-                    if (MM % 2 == 0) put16(MM, 0u);
-                    continue;
-                }
-                const uint64_t key = rmfht_maps::slot_key(prm.seed, prm.frame0 + (long long)q, at, s);
-                if (mn == MM) {
-                    rmfht_maps::draw_store<MM, MM>(key, put, put16);
-                } else if constexpr (MM > 2) {
-                    if (mn == MM - 1) {
-                        rmfht_maps::draw_store<MM - 1, MM>(key, put, put16);
-                    } else {
-                        uint32_t tmp[W];
-                        rmfht_maps::draw_store_rt<MM>(key, mn, tmp);
-#pragma unroll
-                        for (int k = 0; k < W; k++) dst[k] = tmp[k];
-                    }
-                }
-            }
-        } else {
-            // the round's items are consecutive: copy each item's S records
-            constexpr int RB = S * W * 4;  // bytes per item
-            constexpr int CH = RB % 16 == 0 ? 16 : RB % 8 == 0 ? 8 : 4;
-            constexpr int NC = RB / CH;
-            const bool al = (reinterpret_cast<uintptr_t>(prm.maps) & (CH - 1)) == 0;
-#pragma unroll 1
-            for (int t = lane; t < nwarps * NC; t += 32) {
-                const int w = t / NC, c = t - (t / NC) * NC;
-                const int item = base + w;
-                if (item >= items) continue;
-                const char* g = reinterpret_cast<const char*>(prm.maps) + (size_t)item * RB + c * CH;
-                const u32 sa = (u32)__cvta_generic_to_shared(wsarr[w].recs[buf]) + c * CH;
-                if (CH == 16 && al) {
-                    cp_async16(sa, g);
-                } else {
-#pragma unroll
-                    for (int b = 0; b < CH; b += 4) cp_async4(sa + b, g + b);
-                }
-            }
-            cp_async_commit();
-            cp_async_wait_all();
-        }
-    }
-}
-
-// Work item = (frame, attempt); the decoding warps of a CTA take consecutive
-// items in lock-stepped rounds (they run the same code path, so they share
-// the instruction stream); warp 0 produces the next round's map records.
+// Work item = (frame, attempt); warps of a CTA take consecutive items in
+// lock-stepped rounds (they run the same code path, so they share the
+// instruction stream).
 // PM: permutations (p-FHT-FSCL); false = FHT-FSC (L = 1, identity maps)
 template <int R, int MM, int L, bool PM = true>
 #ifdef RMFHT_FAST_LB_WARPS
 #define RMFHT_KERNEL2_LB (32 * RMFHT_FAST_LB_WARPS)  // A/B builds only: register cap of a larger CTA
 #else
-#define RMFHT_KERNEL2_LB (32 * (fast_warps<R, MM, L>() + 1))
+#define RMFHT_KERNEL2_LB (32 * fast_warps<R, MM, L>())
 #endif
 __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Params<float> prm, AttHdr* hdr, u64* bitsout) {
     using C = Cfg<R, MM, L>;
     using WS = WS2<R, MM, L>;
     using LV = Lv<MM, C::LPP>;
-    constexpr int N = C::N, V = LV::V;
+    constexpr int N = C::N, S = C::S, REC = 2 * MM + 2, V = LV::V;
     static_assert(N >= 32 && L <= 8 && N <= 512, "fast kernel: 32 <= N <= 512, L <= 8");
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    // the launch always uses fast_warps() decoding warps + the producer
-    // (prepare_fast): a compile-time count keeps the per-warp scratch
-    // addresses cheap to rematerialise
+    // the launch always uses fast_warps() warps (prepare_fast): a compile-time
+    // count keeps the per-warp scratch addresses cheap to rematerialise
     constexpr int nwarps = fast_warps<R, MM, L>();
-    const int lane = lane_id();
+    const int warp = threadIdx.x >> 5, lane = lane_id();
     // per-warp frame LLRs, each 2 KB aligned in the shared window, then the scratch
     const u32 raw_saddr = (u32)__cvta_generic_to_shared(smem_raw);
     const u32 pad = ((raw_saddr + 2047u) & ~2047u) - raw_saddr;
     constexpr u32 ASTRIDE = (u32)N * 4u;  // N-aligned: gather offsets (< 4N bytes) are OR-ed into the base
+    float* const alpha_w = reinterpret_cast<float*>(smem_raw + pad + (size_t)warp * ASTRIDE);
     WS* wsarr = reinterpret_cast<WS*>(smem_raw + pad + (size_t)nwarps * ASTRIDE);
+    WS& ws = wsarr[warp];
+    const u32 asa = (u32)__cvta_generic_to_shared(alpha_w);
+    Ctx2<R, MM, L> cx{ws, alpha_w, nullptr, PM ? 1 : 0, {}, lane, lane / C::LPP, lane % C::LPP, asa};
     static_assert(sizeof(MapR<MM>) == 2 * (2 * MM + 2), "record layout");
     constexpr bool ROOT_INTERNAL = !(R == 1 || R == MM - 1);
     // items < 2^31 per launch (launch_fast splits larger batches)
     const int items = (int)prm.B * prm.M;
     const int stride = (int)gridDim.x * nwarps;
-    if (threadIdx.x < 32) {
-        // ---- record producer: one barrier per round, like the decoding warps
-        int cur = 0;
-        produce_round<R, MM, L, PM>(prm, wsarr, (int)blockIdx.x * nwarps, 0, items, lane);
-        __syncthreads();
-        for (int base = (int)blockIdx.x * nwarps; base < items; base += stride) {
-            produce_round<R, MM, L, PM>(prm, wsarr, base + stride, cur ^ 1, items, lane);
-            __syncthreads();
-            cur ^= 1;
+    // Prefetch (LDGSTS) of the warp's next work item: its map records into the
+    // idle half of ws.recs at item start, its LLRs into the single LLR buffer
+    // as soon as the current item has read the frame LLRs for the last time
+    // (after the root's g, i.e. before the right half of the tree).
+    auto prefetch_recs = [&](int it, int buf) {
+        if (it >= items || !PM) return;
+        const u32 rsa = (u32)__cvta_generic_to_shared(ws.recs[buf]);
+        const char* gr = reinterpret_cast<const char*>(prm.maps + (size_t)it * S * REC);
+        constexpr int RB = S * REC * 2;  // record bytes per item
+        if (RB % 16 == 0 && (reinterpret_cast<uintptr_t>(prm.maps) & 15u) == 0) {
+            for (int i = lane; i < RB / 16; i += 32) cp_async16(rsa + 16u * i, gr + 16 * i);
+        } else {
+            for (int i = lane; i < WS::RECW / 2; i += 32) cp_async4(rsa + 4u * i, gr + 4 * i);
         }
-        return;
-    }
-    const int warp = (threadIdx.x >> 5) - 1;
-    float* const alpha_w = reinterpret_cast<float*>(smem_raw + pad + (size_t)warp * ASTRIDE);
-    WS& ws = wsarr[warp];
-    const u32 asa = (u32)__cvta_generic_to_shared(alpha_w);
-    Ctx2<R, MM, L> cx{ws, alpha_w, nullptr, PM ? 1 : 0, {}, lane, lane / C::LPP, lane % C::LPP, asa};
-    // LLR prefetch (LDGSTS) of the warp's next work item into its single LLR
-    // buffer as soon as the current item has read the frame LLRs for the
-    // last time (after the root's g, i.e. before the right half of the tree)
+        cp_async_commit();
+    };
     auto prefetch_alpha = [&](int it) {
         if (it >= items) return;
         __syncwarp();  // every lane is past its last read of the current LLRs
@@ -1738,8 +1648,8 @@ __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Par
         cp_async_commit();
     };
     int cur = 0;
+    prefetch_recs((int)blockIdx.x * nwarps + warp, 0);
     prefetch_alpha((int)blockIdx.x * nwarps + warp);
-    __syncthreads();  // round 0's records
     for (int base = (int)blockIdx.x * nwarps; base < items; base += stride) {
         const int item = base + warp;
         if (item < items) {
@@ -1749,6 +1659,7 @@ __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Par
 #endif
             cp_async_wait_all();
             __syncwarp();
+            prefetch_recs(item + stride, cur ^ 1);
 #pragma unroll
             for (int s = 0; s < C::NS; s++) cx.ach[s] = alpha_w[lane + 32 * s];
             cx.maps = reinterpret_cast<const MapR<MM>*>(ws.recs[cur]);
@@ -1788,30 +1699,17 @@ __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Par
             for (int i = 1; i < L; i++)
                 if (ws.pm[i] < ws.pm[best]) best = i;
             const int rslot = ROOT_INTERNAL ? ws.rootchain[best] : rlin[best];
-            // its forward composite root map sigma = trial o init, one column
-            // per lane (lane m: the shift): A_t (A_i e_k) and A_t b_i ^ b_t
-            if (lane <= MM) {
-                u32 x = lane < MM ? (1u << lane) : 0u;
-                if constexpr (PM) {
-                    const int im = ROOT_INTERNAL ? ws.l0[MM][rslot] : rslot;
-                    x = reinterpret_cast<const uint16_t*>(&cx.maps[im])[lane];  // col[lane] or b (half word MM)
-                    if constexpr (ROOT_INTERNAL) {
-                        const uint16_t* tr = reinterpret_cast<const uint16_t*>(&cx.maps[ws.nmap[MM][rslot]]);
-                        u32 v = lane == MM ? (u32)tr[MM] : 0u;
-#pragma unroll
-                        for (int j = 0; j < MM; j++)
-                            if ((x >> j) & 1u) v ^= tr[j];
-                        x = v;
-                    }
-                }
-                hdr[item].fwd[lane] = (uint16_t)x;
-            }
             if (lane == 0) {
-                hdr[item].pm = ws.pm[best];
-                hdr[item].path = best;
+                AttHdr h;
+                h.pm = ws.pm[best];
+                h.path = best;
+                h.init_map = !PM ? -1 : ROOT_INTERNAL ? ws.l0[MM][rslot] : rslot;
+                h.trial_map = !PM ? -1 : ROOT_INTERNAL ? ws.nmap[MM][rslot] : -1;
+                hdr[item] = h;
             }
             if (cx.p == best) bitsout[(size_t)item * C::LPP + cx.u] = bits;
             __syncwarp();
+            cur ^= 1;
 #ifdef RMFHT_STATS
             {
                 const long long dt = clock64() - t_item;
@@ -1827,10 +1725,13 @@ __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Par
             }
 #endif
         }
-        // lock-step rounds: the decoding warps share the instruction stream,
-        // and the producer's records for the next round become visible
-        __syncthreads();
-        cur ^= 1;
+        // lock-step rounds: warps share the instruction stream (named barrier per group)
+        const int grp = (prm.tie_fix >> 8) & 0xff;  // warps per lock-step group, 0 = none
+        if (grp >= nwarps || nwarps % grp != 0) {
+            __syncthreads();
+        } else if (grp > 0) {
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + warp / grp), "r"(grp * 32) : "memory");
+        }
     }
 }
 
@@ -1840,7 +1741,7 @@ __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Par
 template <int R, int MM, int L>
 __global__ void __launch_bounds__(256) reduce_kernel2(rmfht::Params<float> prm, const AttHdr* hdr, const u64* bitsin) {
     using C = Cfg<R, MM, L>;
-    constexpr int N = C::N, NW = N / 32, LPP = C::LPP;
+    constexpr int N = C::N, NW = N / 32, S = C::S, REC = 2 * MM + 2, LPP = C::LPP;
     __shared__ u64 sbits[8][LPP];
     __shared__ MapS smap[8];
     const int warp = threadIdx.x >> 5, lane = lane_id();
@@ -1866,9 +1767,27 @@ __global__ void __launch_bounds__(256) reduce_kernel2(rmfht::Params<float> prm, 
         const long long item = f * M + a;
         const AttHdr h = hdr[item];
         if (lane < LPP) sbits[warp][lane] = bitsin[(size_t)item * LPP + lane];
-        // the attempt's forward composite root map (decode_kernel2 epilogue)
-        if (lane < MM) smap[warp].col[lane] = h.fwd[lane];
-        else if (lane == MM) smap[warp].b = h.fwd[MM];
+        // the winner's composite sigma = trial o init (columns of A and the
+        // shift), one column per lane: lane k < MM takes column k, lane MM the
+        // shift — A_t (A_i e_k) and A_t b_i ^ b_t
+        if (lane <= MM) {
+            u32 x;
+            if (h.init_map < 0) {  // no permutations: identity
+                x = lane < MM ? (1u << lane) : 0u;
+            } else {
+                x = prm.maps[((size_t)item * S + h.init_map) * REC + lane];  // col[lane] or b (half word MM)
+            }
+            if (h.trial_map >= 0) {
+                const uint16_t* tr = prm.maps + ((size_t)item * S + h.trial_map) * REC;
+                u32 v = lane == MM ? (u32)tr[MM] : 0u;
+#pragma unroll
+                for (int j = 0; j < MM; j++)
+                    if ((x >> j) & 1u) v ^= tr[j];
+                x = v;
+            }
+            if (lane < MM) smap[warp].col[lane] = x;
+            else smap[warp].b = x;
+        }
         __syncwarp();
         const MapS& fm = smap[warp];
         u32 myword = 0;

@@ -20,8 +20,7 @@ size_t smem_of(const rmfht_plan* p, int nw) {
 
 template <typename T>
 int launch_gen(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint32_t* cw, void* pm, int32_t* att,
-               int32_t* path, void* att_pm, uint32_t* att_cw, long long B,
-           const rmfht_sample_spec* /*table in maps*/, void* /*work: none*/, cudaStream_t st) {
+               int32_t* path, void* att_pm, uint32_t* att_cw, long long B, void* /*work: none*/, cudaStream_t st) {
     rmfht::Params<T> prm;
     prm.llr = static_cast<const T*>(llr);
     prm.maps = maps;

@@ -150,13 +150,6 @@ struct Params {
     int32_t* path;         // [B]
     T* att_pm;             // optional [B, M]
     uint32_t* att_cw;      // optional [B, M, N/32]
-    // on-device tables (throughput kernel): maps == nullptr and sampled != 0
-    // -> the kernel's record-producer warp draws slot (f, a, s) from
-    // slot_key(seed, frame0 + f, a, s) (rmfht_maps.cuh), bit-identical to
-    // rmfht_sample_maps
-    unsigned long long seed = 0;
-    long long frame0 = 0;
-    int sampled = 0, identity_root = 0;
 };
 
 template <typename T, int R, int MM, int L>

@@ -269,57 +269,4 @@ inline void fill_slot_host_any(int mn, uint64_t key, int mg, uint16_t* raw, uint
     }
 }
 
-#ifdef __CUDACC__
-// ---- device record writers (the sampler kernel and the decoder's record
-// producer warp share them, so both give the host table bit for bit)
-// one record (2MG+2 uint16 = MG+1 words): word w handed to put(w, value),
-// then the columns of A^-1 and A^-1 b as half words put16(half, value) — a
-// basis word's pivot names the column it holds (draw_map_basis), so the
-// columns land at their half-word slots with no register permutation
-template <int MN, int MG, typename Put, typename Put16>
-__device__ __forceinline__ void draw_store(uint64_t key, Put&& put, Put16&& put16) {
-    unsigned cols[MN], ub[MN], pv[MN], b;
-    rmfht_maps::draw_map_basis<MN>(key, cols, ub, pv, b);
-    // record halves: cols of A (MG), b, cols of A^-1 (MG), A^-1 b; whole
-    // words up to half MG, half words after (never both on one location)
-    unsigned h[MG + 2];
-#pragma unroll
-    for (int k = 0; k < MG + 2; k++) h[k] = 0u;
-#pragma unroll
-    for (int k = 0; k < MN; k++) h[k] = cols[k];
-    h[MG] = b;
-    constexpr int WF = (MG + 1) / 2;  // words made of halves 0 .. 2 WF - 1 <= MG
-#pragma unroll
-    for (int w = 0; w < WF; w++) put(w, h[2 * w] | (h[2 * w + 1] << 16));
-    if constexpr (2 * WF == MG) put16(MG, b);
-#pragma unroll
-    for (int k = MN; k < MG; k++) put16(MG + 1 + k, 0u);
-    unsigned c = 0u;
-#pragma unroll
-    for (int j = 0; j < MN; j++) {
-        const unsigned coef = ub[j] >> 16;
-        put16(MG + 1 + (__ffs(pv[j]) - 1), coef);
-        if (b & pv[j]) c ^= coef;  // A^-1 b = sum over the set bits k of b of column k
-    }
-    put16(2 * MG + 1, c);
-}
-
-// slots below MG-2 variables (r >= 5)
-template <int MG>
-__device__ __noinline__ void draw_store_rt(uint64_t key, int mn, uint32_t* o) {
-    unsigned cols[16], icols[16], b;
-    rmfht_maps::draw_map_rt(key, mn, cols, icols, b);
-    unsigned cinv = 0, h[2 * MG + 2];
-    for (int k = 0; k < MG; k++) {
-        h[k] = k < mn ? cols[k] : 0u;
-        h[MG + 1 + k] = k < mn ? icols[k] : 0u;
-        if (k < mn && ((b >> k) & 1u)) cinv ^= icols[k];
-    }
-    h[MG] = b;
-    h[2 * MG + 1] = cinv;
-    for (int w = 0; w <= MG; w++) o[w] = h[2 * w] | (h[2 * w + 1] << 16);
-}
-
-#endif  // __CUDACC__
-
 }  // namespace rmfht_maps

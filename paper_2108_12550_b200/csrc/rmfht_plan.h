@@ -10,16 +10,9 @@
 
 #include "../../include/rmfht.h"
 
-// on-device table of a sampled launch (rmfht_decode_launch_sampled)
-struct rmfht_sample_spec {
-    unsigned long long seed;
-    long long frame0;
-    int identity_root;
-};
-// the last pointers: on-device sampling (NULL: table in d_maps), and the
-// caller-owned device workspace (rmfht_workspace_bytes)
+// the last pointer is the caller-owned device workspace (rmfht_workspace_bytes)
 using LaunchFn = int (*)(const rmfht_plan*, const void*, const uint16_t*, uint32_t*, void*, int32_t*,
-                         int32_t*, void*, uint32_t*, long long, const rmfht_sample_spec*, void*, cudaStream_t);
+                         int32_t*, void*, uint32_t*, long long, void*, cudaStream_t);
 using PrepareFn = int (*)(rmfht_plan*);
 
 struct rmfht_plan {
@@ -40,9 +33,6 @@ struct rmfht_plan {
     // throughput kernel: per-(frame, attempt) bytes of the caller-owned
     // workspace (rmfht_workspace_bytes); 0 for kernels that need none
     size_t work_per_item = 0;
-    // the kernel draws its own tables (throughput kernel's producer warp):
-    // sampled launches need no table in the workspace and no sampler kernel
-    int fused_sampling = 0;
 };
 
 // workspace helpers shared by the C-ABI unit and the binding units

@@ -307,8 +307,7 @@ int prepare_reg(rmfht_plan* p) {
 
 template <typename T, int R, int MM>
 int launch_reg(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint32_t* cw, void* pm, int32_t* att,
-               int32_t* path, void* att_pm, uint32_t* att_cw, long long B,
-           const rmfht_sample_spec* /*table in maps*/, void* /*work: none*/, cudaStream_t st) {
+               int32_t* path, void* att_pm, uint32_t* att_cw, long long B, void* /*work: none*/, cudaStream_t st) {
     rmfht::Params<T> prm;
     prm.llr = static_cast<const T*>(llr);
     prm.maps = maps;
@@ -354,8 +353,7 @@ int prepare(rmfht_plan* p) {
 
 template <typename T>
 int launch(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint32_t* cw, void* pm, int32_t* att,
-           int32_t* path, void* att_pm, uint32_t* att_cw, long long B,
-           const rmfht_sample_spec* /*table in maps*/, void* /*work: none*/, cudaStream_t st) {
+           int32_t* path, void* att_pm, uint32_t* att_cw, long long B, void* /*work: none*/, cudaStream_t st) {
     rmfht::Params<T> prm;
     prm.llr = static_cast<const T*>(llr);
     prm.maps = maps;
