@@ -158,7 +158,8 @@ int rmfht_plan_launches_per_call(const rmfht_plan *plan);
 
 /* Which kernel the plan runs: 1 = reference-order (rmfht_kernels.cuh),
  * 2 = float32 throughput kernel (rmfht_fast.cuh), 3 = generic runtime-shaped
- * kernel (rmfht_generic.cuh, reference order), 4 = Aut-SSC (rmfht_ssc.cu);
+ * kernel (rmfht_generic.cuh, reference order), 4 = Aut-SSC (rmfht_ssc.cu),
+ * 5 = lane-per-frame FHT-FSC kernel for N <= 64 (rmfht_lane.cuh);
  * 0 for a NULL plan. */
 int rmfht_plan_kernel(const rmfht_plan *plan);
 

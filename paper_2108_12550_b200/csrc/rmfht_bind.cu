@@ -4,6 +4,7 @@
 
 #include "rmfht_fast.cuh"
 #include "rmfht_kernels.cuh"
+#include "rmfht_lane.cuh"
 #include "rmfht_plan.h"
 
 #ifndef RMFHT_T
@@ -150,8 +151,59 @@ int prepare_fast(rmfht_plan* p) {
     return 0;
 }
 
+// lane-per-frame kernel (rmfht_lane.cuh): FHT-FSC on short codes
+template <int R, int MM>
+int launch_lane(const rmfht_plan* p, const void* llr, const uint16_t* /*maps*/, uint32_t* cw, void* pm, int32_t* att,
+                int32_t* path, void* att_pm, uint32_t* att_cw, long long B, void* /*work: none*/, cudaStream_t st) {
+    rmfht::Params<float> prm;
+    prm.llr = static_cast<const float*>(llr);
+    prm.maps = nullptr;
+    prm.B = B;
+    prm.M = 1;
+    prm.perms = 0;
+    prm.tie_fix = 0;
+    prm.cw = cw;
+    prm.pm = static_cast<float*>(pm);
+    prm.attempt = att;
+    prm.path = path;
+    prm.att_pm = static_cast<float*>(att_pm);
+    prm.att_cw = att_cw;
+    if (B <= 0) return 0;
+    auto* mp = const_cast<rmfht_plan*>(p);
+    std::call_once(mp->once, [mp] { mp->prepared_rc = mp->prepare(mp); });
+    if (p->prepared_rc != 0) return p->prepared_rc;
+    const long long blocks = (B + 255) / 256;
+    const long long grid = blocks < p->grid ? blocks : p->grid;
+    rmfht_lane::lane_kernel<R, MM><<<(unsigned)grid, 256, 0, st>>>(prm);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(RMFHT_ECUDA, std::string("lane kernel launch: ") + cudaGetErrorString(e));
+    return 0;
+}
+
+template <int R, int MM>
+int prepare_lane(rmfht_plan* p) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rmfht_lane::lane_kernel<R, MM>, 256, 0);
+    if (e != cudaSuccess || per_sm < 1) return fail(RMFHT_ECUDA, "lane kernel does not fit an SM");
+    p->nwarps = 8;
+    p->smem = 0;
+    p->grid = sms * per_sm;
+    return 0;
+}
+
 template <typename T, int R, int MM, int L>
 int bind_one(rmfht_plan* p) {
+    if constexpr (sizeof(T) == 4 && L == 1 && (1 << MM) <= 64 && (1 << MM) >= 4) {
+        // FHT-FSC (L = 1, no permutations) on a short code: one thread per frame
+        if (p->fast && !p->perms) {
+            p->lane = 1;
+            p->launch = &launch_lane<R, MM>;
+            p->prepare = &prepare_lane<R, MM>;
+            return 0;
+        }
+    }
     if constexpr (sizeof(T) == 4 && (1 << MM) >= 32 && L <= 8) {
         // without permutations the list starts from one path and grows, which
         // the throughput kernel (P == L at every node) does not model: FHT-FSC

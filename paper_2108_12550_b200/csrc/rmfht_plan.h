@@ -20,6 +20,7 @@ struct rmfht_plan {
     int lockstep = 255;  // throughput kernel: warps per lock-step group (0 = none, >= CTA warps = whole CTA)
     int fast;  // float32 throughput kernel (rmfht_fast.cuh) instead of the reference-order one
     int generic = 0;  // runtime-shaped interpreter kernel (rmfht_generic.cuh)
+    int lane = 0;     // lane-per-frame kernel (rmfht_lane.cuh): FHT-FSC on N <= 64
     int force_generic = 0;
     int aut = 0;  // Aut-SSC plan (RMFHT_AUT_SSC): M = P single-map SSC decodes per frame
     int S, nwarps, grid;
