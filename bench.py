@@ -57,7 +57,7 @@ CONFIGS = {
     "rm27_L2_M4": (2, 7, 2, 4, True, 2.0, 262144),
     "rm37_L8_M32": (3, 7, 8, 32, True, 4.0, 16384),
     "rm29_L1_M512": (2, 9, 1, 512, True, 3.0, 1024),
-    "rm25_fhtfsc": (2, 5, 1, 1, False, 3.0, 1048576),
+    "rm25_fhtfsc": (2, 5, 1, 1, False, 3.0, 4194304),
     # the paper's Table IV comparator, Aut-SSC with P = 512 (M = P here)
     "rm29_autssc_P512": (2, 9, 1, 512, "aut", 2.5, 2048),
 }
@@ -132,7 +132,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -142,6 +142,13 @@ class Clocks:
     def _read(self):
         for line in self.proc.stdout:
             self.rows.append([c.strip() for c in line.split(",")])
+
+    def wait_first(self, timeout: float = 3.0):
+        """Block until nvidia-smi has delivered its first row (its start-up
+        takes longer than a short timed region)."""
+        t0 = time.time()
+        while self.proc is not None and not self.rows and time.time() - t0 < timeout:
+            time.sleep(0.02)
 
     def __exit__(self, *a):
         if self.proc is not None:
@@ -397,7 +404,8 @@ def run_gpu(args):
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
-        time.sleep(0.3)
+        clk.wait_first()
+        time.sleep(0.1)
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
@@ -480,21 +488,33 @@ def run_gpu(args):
                        "fer_check": fer_warm},
             "e2e": {"value": e2e, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps": e_steps},
-            "gpu_launches": args.steps * (plan.launches_per_call + 1),
+            # sampler kernel + decode (+ reduce) per step; plans without
+            # permutations launch the decoder alone
+            "gpu_launches": args.steps * (plan.launches_per_call + (1 if PERMS else 0)),
             "decode_only": {"value": ws * B * args.steps / (ms_dec / 1e3), "ms_per_step": ms_dec / args.steps,
                             "note": "same batch, permutation table already resident in HBM"},
-            "roofline": {"bound": "fp32", "achieved": ach_gops, "peak": peak_gops, "unit": "Gop/s",
-                         "frac": ach_gops / peak_gops, "traffic": _traffic(args.config, B),
-                         "ops_per_frame": ops,
-                         "kernel_ms": ms_dec / args.steps,
-                         "note": f"reference op ledger per frame x frames per launch / decode-kernel time (CUDA "
-                                 f"events) vs {sms} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz ({src} sm_max_mhz)"},
-            "roofline_hbm": {"bound": "hbm", "achieved": (bytes_frame + rec_bytes_frame) * kern_fps / 1e9,
-                             "peak": hbm, "unit": "GB/s",
-                             "frac": (bytes_frame + rec_bytes_frame) * kern_fps / 1e9 / hbm,
-                             "bytes_per_frame": bytes_frame + rec_bytes_frame},
+            "roofline_fp32": {"bound": "fp32", "achieved": ach_gops, "peak": peak_gops, "unit": "Gop/s",
+                              "frac": ach_gops / peak_gops, "traffic": _traffic(args.config, B),
+                              "ops_per_frame": ops,
+                              "kernel_ms": ms_dec / args.steps,
+                              "note": f"reference op ledger per frame x frames per launch / decode-kernel time "
+                                      f"(CUDA events) vs {sms} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz ({src} "
+                                      f"sm_max_mhz)"},
+            "roofline_hbm": {"bound": "hbm", "achieved": bytes_frame * kern_fps / 1e9,
+                             "peak": hbm, "unit": "GB/s", "frac": bytes_frame * kern_fps / 1e9 / hbm,
+                             "bytes_per_frame": bytes_frame, "traffic": _traffic(args.config, B),
+                             "note": "LLR-in / codeword-out bytes per frame (4N + N/8) x frames per launch / "
+                                     "decode-kernel time vs MEASURED_PEAKS hbm_gbs; with a host table the kernel "
+                                     f"also reads {rec_bytes_frame} B/frame of map records"},
             "clocks": clk,
         }
+        # the roofline that bounds this config: the slower of the ledger ops at
+        # the FP32 issue peak and the LLR-in / codeword-out bytes at HBM
+        # bandwidth (BASELINE.json north_star)
+        fp32_fps = peak_gops * 1e9 / ops
+        hbm_fps = hbm * 1e9 / bytes_frame
+        line["roofline"] = dict(line["roofline_fp32"] if fp32_fps <= hbm_fps else line["roofline_hbm"])
+        line["roofline"]["bound_frames_per_s"] = min(fp32_fps, hbm_fps)
         cap = _capture(args.config)
         if "warp_instructions" in cap:
             # issue view of the same kernel: warp instructions per frame (ncu,

@@ -1,7 +1,7 @@
 """Lane-per-frame FHT-FSC kernel (rmfht_lane.cuh, plan kernel 5): bit-exact
 with the float32 oracle (codeword, reported pm, attempt, path) on batches
 of every compiled short shape, and equal to the float64 reference port's
-codewords (FHT-FSC decisions do not depend on summation order)."""
+codewords except on float32 near-ties."""
 import numpy as np
 import pytest
 
@@ -24,8 +24,11 @@ def test_lane_kernel_matches_oracle(r, m, ebn0, oracle_mod):
     assert np.array_equal(o["pm"], c["pm"])
     assert not o["attempt"].any() and not o["path"].any()
     assert np.array_equal(o["att_pm"][:, 0], o["pm"]) and np.array_equal(o["att_cw"][:, 0], o["cw"])
+    # the float64 reference port: the same codewords except on float32 near-ties
+    # of the FHT bin / SPC order (selection margin <= 1e-5, oracle/ties.py)
     c64 = oracle_mod.decode(r, m, 1, 1, llr.astype(np.float64), None, perms=False, dtype=np.float64, nthreads=16)
-    assert np.array_equal(o["cw"], c64["cw"])
+    differ = np.any(o["cw"] != c64["cw"], axis=1)
+    assert np.all(c64["margin"][differ] <= 1e-5) and differ.sum() <= 20
     for f in range(0, 20000, 2000):
         assert is_codeword(spec, o["cw"][f])
 
