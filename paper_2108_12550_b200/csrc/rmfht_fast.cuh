@@ -135,14 +135,20 @@ template <int R, int MM, int L>
 struct alignas(16) WS2 {
     using C = Cfg<R, MM, L>;
     static constexpr int RECW = (C::S > 0 ? C::S : 1) * (2 * MM + 2);  // uint16 per item's map records
-    alignas(16) uint16_t recs[2][(RECW + 7) & ~7];  // double-buffered (cp.async prefetch); the item's maps
+    // inner permutation nodes (r >= 3) read the item's records deep in the
+    // tree: double-buffered (the next item's are prefetched at item start);
+    // otherwise the records are dead after the root's permutation extension
+    // and one buffer is refilled from there
+    static constexpr bool INNER = R >= 3 && MM - R >= 2;
+    static constexpr int RB = INNER ? 2 : 1;
+    alignas(16) uint16_t recs[RB][(RECW + 7) & ~7];  // cp.async prefetch; the item's maps
     MapR<MM> comp[L];  // composite map of each root path (root perm-ext winners)
     float pm[L], llrabs[L];
     float lm[2 * L];
     static constexpr int CA = kCap > L * L ? kCap : L * L;  // candidate list (and the exact fallback)
     static constexpr int CB = L * L > 2 * L ? L * L : 2 * L;  // per path / per split / fallback pool
-    float ca[CA], cw[CA], cpm[CB];
-    int cb[CB], cp[CB], celig[CB];
+    float cw[CA], cpm[CB];  // candidate values (|w| = fabsf(cw)), pool pms
+    int16_t cb[CB], cp[CB], celig[CB];
     alignas(16) u64 ckey[kCap + 4];
     // FHT outputs spilled for candidate extraction: lane-major, padded (conflict-free STS.128)
     // largest FHT node: RM(1, m-r+1), the first left descendant (the root when r == 1).
@@ -152,11 +158,20 @@ struct alignas(16) WS2 {
     // The inner permutation nodes' vectors (vbuf, at the node's start) and
     // output bits (ubits, at its end) are dead whenever an FHT node runs, so
     // they share the space too; the largest inner node has N/2 elements.
+    // The SPC nodes' scratch (magnitudes, signs, order of the tau+1 least
+    // reliable positions) is dead whenever any of the others is live: SPC
+    // nodes are leaves that run after an FHT node's spill rows died and
+    // between an inner permutation node's vbuf (its start) and ubits (its end).
     union alignas(16) {
         float wsp[32][VMAX];  // 16-byte chunks XOR-swizzled per lane (wsp_idx): conflict-free STS.128
         float lmp[2 * L][32];
         float vbuf[R >= 3 ? L * C::N / 2 : 1];
         uint8_t ubits[R >= 3 ? L * C::N / 2 : 1];
+        struct {
+            float smag[L * (C::SPCMAX > 16 ? C::SPCMAX : 16)];
+            uint8_t ssgn[L * C::SPCMAX];
+            uint16_t sord[L * 16];
+        };
     };
     // element k of lane `lane`'s row
     // t: extra per-node chunk twist (FhtLayout::twist) for the transposed FHT reads
@@ -170,10 +185,6 @@ struct alignas(16) WS2 {
     float sel_w[2 * L], sel_pm[2 * L];
     int8_t l0[MM + 1][L], l1[MM + 1][L], l2[MM + 1][L], rootchain[L], ord[2 * L];
     int16_t nmap[MM + 1][L];
-    // SPC scratch: magnitudes, signs, order of the tau+1 least reliable positions
-    float smag[L * (C::SPCMAX > 16 ? C::SPCMAX : 16)];
-    uint8_t ssgn[L * C::SPCMAX];
-    uint16_t sord[L * 16];
     int next_map;
 };
 
@@ -394,7 +405,6 @@ __device__ __noinline__ void fht_fallback(WS2<R, MM, L>* wsp_, int lane, float l
             }
             if (act && FL::owner(bb) == u) taken |= 1ull << FL::slot(bb);
             if (u == 0) {
-                ws.ca[p * K + rr] = bv;
                 ws.cb[p * K + rr] = bb;
                 ws.cw[p * K + rr] = bw;
                 ws.cp[p * K + rr] = p;
@@ -402,7 +412,7 @@ __device__ __noinline__ void fht_fallback(WS2<R, MM, L>* wsp_, int lane, float l
         }
         __syncwarp();
         constexpr int PK = L * K;
-        for (int c = lane; c < PK; c += 32) ws.cpm[c] = ws.pm[c / K] + 0.5f * (ws.llrabs[c / K] - ws.ca[c]);
+        for (int c = lane; c < PK; c += 32) ws.cpm[c] = ws.pm[c / K] + 0.5f * (ws.llrabs[c / K] - fabsf(ws.cw[c]));
         __syncwarp();
 #pragma unroll 1
         for (int c = lane; c < PK; c += 32) {
@@ -462,8 +472,8 @@ __device__ __noinline__ void fht_exact(WS2<R, MM, L>* wsp_, int lane, u64 mask64
         // this path's candidates occupy [pstart, pstart + pcnt) (lane order)
         const int pstart = __shfl_sync(kFull, incl - cnt, p * C::LPP);
         if (u == 0) {
-            ws.cp[p] = pstart;
-            ws.celig[p] = pcnt;
+            ws.cp[p] = (int16_t)pstart;
+            ws.celig[p] = (int16_t)pcnt;
         }
         MaskT mk = mask;
         while (mk) {
@@ -476,7 +486,6 @@ __device__ __noinline__ void fht_exact(WS2<R, MM, L>* wsp_, int lane, u64 mask64
             u32 kb = __float_as_uint(pmc);
             kb ^= (kb >> 31) ? 0xffffffffu : 0x80000000u;  // order-preserving for any sign
             ws.ckey[pos] = ((u64)kb << 32) | ((u32)p << 16) | (u32)bin;
-            ws.ca[pos] = a;
             ws.cw[pos] = v;
             pos++;
         }
@@ -494,11 +503,11 @@ __device__ __noinline__ void fht_exact(WS2<R, MM, L>* wsp_, int lane, u64 mask64
                     const int pi = (int)((ki >> 16) & 0xffff), bi = (int)(ki & 0xffff);
                     const int j0 = ws.cp[pi], j1 = j0 + ws.celig[pi];
                     if (j1 - j0 > K) {
-                        const float ai = ws.ca[i];
+                        const float ai = fabsf(ws.cw[i]);
                         int rp = 0;
 #pragma unroll 1
                         for (int j = j0; j < j1; j++) {
-                            const float aj = ws.ca[j];
+                            const float aj = fabsf(ws.cw[j]);
                             rp += aj > ai || (aj == ai && (int)(ws.ckey[j] & 0xffff) < bi);
                         }
                         kill[h] = rp >= K;
@@ -1659,7 +1668,7 @@ __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Par
 #endif
             cp_async_wait_all();
             __syncwarp();
-            prefetch_recs(item + stride, cur ^ 1);
+            if constexpr (WS::RB == 2) prefetch_recs(item + stride, cur ^ 1);
 #pragma unroll
             for (int s = 0; s < C::NS; s++) cx.ach[s] = alpha_w[lane + 32 * s];
             cx.maps = reinterpret_cast<const MapR<MM>*>(ws.recs[cur]);
@@ -1682,6 +1691,9 @@ __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Par
             if constexpr (ROOT_INTERNAL) {
                 if constexpr (PM) perm_ext_root2(cx);
             }
+            // single record buffer: the records are dead from here on (the root
+            // maps live on in ws.comp); refill it with the next item's
+            if constexpr (WS::RB == 1) prefetch_recs(item + stride, 0);
             if constexpr (ROOT_INTERNAL && Lv<MM - 1, C::LPP>::full) {
                 bits = root_node(cx, rlin, [&] { prefetch_alpha(item + stride); });
             } else {
@@ -1709,7 +1721,7 @@ __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Par
             }
             if (cx.p == best) bitsout[(size_t)item * C::LPP + cx.u] = bits;
             __syncwarp();
-            cur ^= 1;
+            if constexpr (WS::RB == 2) cur ^= 1;
 #ifdef RMFHT_STATS
             {
                 const long long dt = clock64() - t_item;
