@@ -92,9 +92,9 @@ def select_config(name):
 
 
 def _capture(config):
-    """The dominant kernel's ncu figures for this config (profiles/r1_traffic.json), or {}."""
+    """The dominant kernel's ncu figures for this config (profiles/r2_traffic.json), or {}."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as fh:
             return json.load(fh)[config]
     except Exception:
         return {}
