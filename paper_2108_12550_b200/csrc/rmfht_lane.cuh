@@ -134,17 +134,25 @@ template <int R, int MM>
 __global__ void __launch_bounds__(256) lane_kernel(rmfht::Params<float> prm) {
     constexpr int N = 1 << MM, NW = N >= 32 ? N / 32 : 1;
     static_assert(N >= 4 && N <= 64, "lane kernel: 4 <= N <= 64");
-    for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < prm.B;
-         f += (long long)gridDim.x * blockDim.x) {
-        float x[N];
-        const float* src = prm.llr + f * N;
-        if constexpr (N % 4 == 0) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    // software pipeline: the next frame's LLRs are in flight while this one
+    // decodes (the kernel is bound by HBM latency: two frames per thread in
+    // flight double the memory-level parallelism)
+    float4 nxt[N / 4];
+    auto load = [&](long long f) {
+        const float4* src = reinterpret_cast<const float4*>(prm.llr + f * N);
 #pragma unroll
-            for (int k = 0; k < N / 4; k++) {
-                const float4 v = __ldg(reinterpret_cast<const float4*>(src) + k);
-                x[4 * k] = v.x; x[4 * k + 1] = v.y; x[4 * k + 2] = v.z; x[4 * k + 3] = v.w;
-            }
+        for (int k = 0; k < N / 4; k++) nxt[k] = __ldg(src + k);
+    };
+    long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (f < prm.B) load(f);
+    for (; f < prm.B; f += stride) {
+        float x[N];
+#pragma unroll
+        for (int k = 0; k < N / 4; k++) {
+            x[4 * k] = nxt[k].x; x[4 * k + 1] = nxt[k].y; x[4 * k + 2] = nxt[k].z; x[4 * k + 3] = nxt[k].w;
         }
+        if (f + stride < prm.B) load(f + stride);
         const BitsT<MM> bits = node<R, MM>(x);
         // reported pm: rmfht::CorrPm's order, lane l's positions l, l + 32
         double q[32];
