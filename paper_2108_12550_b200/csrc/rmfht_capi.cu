@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(256) sample_kernel(SampleArgs a, uint32_t* rec
     extern __shared__ uint32_t stage[];
     constexpr int W = MG + 1;  // words per record
     const long long items = a.B * (long long)a.M;
-    const int S = a.S, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int S = a.S, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const long long groups = (items + G - 1) / G;
     for (long long g = blockIdx.x; g < groups; g += gridDim.x) {
         const long long item0 = g * G;
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(256) sample_kernel(SampleArgs a, uint32_t* rec
                 at = (int)(item % a.M);
             }
             f += a.frame0;
-            for (int s = warp; s < S; s += 8) {
+            for (int s = warp; s < S; s += nw) {
                 const unsigned o0 = (unsigned)(lane * S + s) * W;
                 auto put = [&](int w, unsigned v) {
                     const unsigned o = o0 + w;
@@ -320,6 +320,11 @@ int rmfht_sample_maps_device(const rmfht_plan* p, uint64_t seed, long long frame
     int G = 32;
     auto stage_bytes = [&](int g) { const size_t t = (size_t)g * p->S * W; return (t + t / 32 + 1) * 4; };
     while (G > 1 && stage_bytes(G) > 48 * 1024) G /= 2;
+    // warps per CTA: the largest divisor of S up to 8, so every warp draws
+    // the same number of slots (S = 12 on 8 warps left 4 warps idle half the time)
+    int nw = 1;
+    for (int d = 8; d >= 1; d--)
+        if (p->S % d == 0) { nw = d; break; }
     const long long groups = (B * (long long)p->M + G - 1) / G;
     long long blocks = groups < 148 * 16 ? groups : 148 * 16;
     const size_t smem = stage_bytes(G);
@@ -328,7 +333,7 @@ int rmfht_sample_maps_device(const rmfht_plan* p, uint64_t seed, long long frame
     switch (p->m) {
 #define RMFHT_SK(K) \
     case K:         \
-        sample_kernel<K><<<(unsigned)blocks, 256, smem, st>>>(a, d_rec32, G); \
+        sample_kernel<K><<<(unsigned)blocks, 32 * nw, smem, st>>>(a, d_rec32, G); \
         break;
         RMFHT_SK(2) RMFHT_SK(3) RMFHT_SK(4) RMFHT_SK(5) RMFHT_SK(6) RMFHT_SK(7) RMFHT_SK(8) RMFHT_SK(9)
         RMFHT_SK(10) RMFHT_SK(11) RMFHT_SK(12) RMFHT_SK(13) RMFHT_SK(14)
