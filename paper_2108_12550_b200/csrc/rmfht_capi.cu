@@ -197,6 +197,8 @@ int rmfht_plan_create(int r, int m, int L, int M, int flags, int dtype, rmfht_pl
     p->force_generic = (flags & RMFHT_GENERIC) ? 1 : 0;
     if (flags & RMFHT_LOCKSTEP_4) p->lockstep = 4;
     if (flags & RMFHT_LOCKSTEP_8) p->lockstep = 8;
+    // A/B experiments only: warps per lock-step group of the throughput kernel
+    if (const char* env = std::getenv("RMFHT_LOCKSTEP_GROUP")) p->lockstep = std::atoi(env) & 0xff;
     if (flags & RMFHT_TIE_FIX) p->tie_fix = 1;
     if (flags & RMFHT_NO_TIE_FIX) p->tie_fix = 0;
     if (flags & RMFHT_AUT_SSC) {
