@@ -169,6 +169,84 @@ __global__ void __launch_bounds__(256) sample_kernel(SampleArgs a, uint32_t* rec
     }
 }
 
+// One thread per map: thread t of the launch draws task t = (item, slot)
+// = (t / S, t % S) of the table (item-major, the record order in memory), so
+// the 32 lanes of a warp draw 32 consecutive records and every thread has
+// exactly one draw — no idle warps, no CTA barrier.  A warp stages its 32
+// records in its own shared-memory rows (record stride W + 1 words: odd,
+// conflict-free) and writes them out as 32 x W contiguous words (coalesced
+// 32-bit stores).  Same draws as sample_kernel (draw_store: bit-identical
+// tables).
+template <int MG>
+__global__ void __launch_bounds__(256) sample_kernel_flat(SampleArgs a, uint32_t* rec) {
+    constexpr int W = MG + 1;
+    __shared__ uint32_t stage[8][32 * (W + 1)];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long tasks = a.B * (long long)a.M * a.S;
+    uint32_t* st = stage[warp];
+    for (long long t0 = ((long long)blockIdx.x * 8 + warp) * 32; t0 < tasks; t0 += (long long)gridDim.x * 256) {
+        const long long t = t0 + lane;
+        if (t < tasks) {
+            long long item;
+            int s;
+            if (t < (1LL << 31)) {
+                const unsigned q = (unsigned)t / (unsigned)a.S;
+                item = q;
+                s = (int)((unsigned)t - q * (unsigned)a.S);
+            } else {
+                item = t / a.S;
+                s = (int)(t % a.S);
+            }
+            long long f;
+            int at;
+            if (item < (1LL << 31)) {
+                const unsigned q = (unsigned)item / (unsigned)a.M;
+                f = q;
+                at = (int)((unsigned)item - q * (unsigned)a.M);
+            } else {
+                f = item / a.M;
+                at = (int)(item % a.M);
+            }
+            f += a.frame0;
+            uint32_t* dst = st + lane * (W + 1);
+            auto put = [&](int w, unsigned v) { dst[w] = v; };
+            auto put16 = [&](int hw, unsigned v) { reinterpret_cast<uint16_t*>(dst)[hw] = (uint16_t)v; };
+            const int mn = a.sizes[s];
+            if (a.identity_root && at == 0 && s < a.L) {
+#pragma unroll
+                for (int w = 0; w < W; w++) {
+                    const unsigned lo = (2 * w < mn) ? 1u << (2 * w) : 0u;
+                    const unsigned hi = (2 * w + 1 < mn) ? 1u << (2 * w + 1) : 0u;
+                    dst[w] = (2 * w < MG ? lo : 0u) | ((2 * w + 1 < MG ? hi : 0u) << 16);
+                }
+                for (int k = 0; k < MG; k++) put16(MG + 1 + k, k < mn ? 1u << k : 0u);
+                put16(2 * MG + 1, 0u);
+                if (MG % 2 == 0) put16(MG, 0u);
+            } else {
+                const uint64_t key = rmfht_maps::slot_key(a.seed, f, at, s);
+                if (mn == MG) draw_store<MG, MG>(key, put, put16);
+                else if (mn == MG - 1 && MG > 1) draw_store<(MG > 1 ? MG - 1 : 1), MG>(key, put, put16);
+                else if (mn == MG - 2 && MG > 2) draw_store<(MG > 2 ? MG - 2 : 1), MG>(key, put, put16);
+                else {
+                    uint32_t tt[W];
+                    draw_store_rt<MG>(key, mn, tt);
+#pragma unroll
+                    for (int w = 0; w < W; w++) put(w, tt[w]);
+                }
+            }
+        }
+        __syncwarp();
+        const long long n = tasks - t0 < 32 ? tasks - t0 : 32;  // records of this warp
+        uint32_t* out = rec + t0 * W;
+#pragma unroll
+        for (int j = 0; j < W; j++) {
+            const int o = j * 32 + lane;  // word o of the warp's n * W words
+            if (o < n * W) out[o] = st[(o / W) * (W + 1) + o % W];
+        }
+        __syncwarp();
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -330,12 +408,26 @@ int rmfht_sample_maps_device(const rmfht_plan* p, uint64_t seed, long long frame
     const long long groups = (B * (long long)p->M + G - 1) / G;
     long long blocks = groups < 148 * 16 ? groups : 148 * 16;
     const size_t smem = stage_bytes(G);
+    // one thread per map (sample_kernel_flat) when every slot has m variables:
+    // consecutive lanes draw consecutive slots, so mixed slot sizes (r >= 3)
+    // would diverge within a warp — those keep the slot-per-warp kernel.
+    // Measured (ncu launch lists): RM(2,9) L4 M20 0.321 -> 0.286 ms, M = 512
+    // L = 1 0.091 -> 0.064 ms, Aut-SSC P512 0.120 -> 0.045 ms; RM(3,7) L8 M32
+    // 0.568 ms slot-per-warp vs 0.899 ms flat.  RMFHT_SAMPLER=group|flat
+    // forces one (A/B only).
+    bool flat = true;
+    for (int s = 0; s < p->S; s++) flat = flat && p->sizes[s] == p->m;
+    if (const char* sv = std::getenv("RMFHT_SAMPLER")) flat = sv[0] == 'f';
+    const long long warps_needed = (B * (long long)p->M * p->S + 31) / 32;
+    const long long fblocks_all = (warps_needed + 7) / 8;
+    const long long fblocks = fblocks_all < (long long)148 * 32 ? fblocks_all : (long long)148 * 32;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     uint32_t* d_rec32 = reinterpret_cast<uint32_t*>(d_rec);
     switch (p->m) {
 #define RMFHT_SK(K) \
     case K:         \
-        sample_kernel<K><<<(unsigned)blocks, 32 * nw, smem, st>>>(a, d_rec32, G); \
+        if (flat) sample_kernel_flat<K><<<(unsigned)fblocks, 256, 0, st>>>(a, d_rec32); \
+        else sample_kernel<K><<<(unsigned)blocks, 32 * nw, smem, st>>>(a, d_rec32, G); \
         break;
         RMFHT_SK(2) RMFHT_SK(3) RMFHT_SK(4) RMFHT_SK(5) RMFHT_SK(6) RMFHT_SK(7) RMFHT_SK(8) RMFHT_SK(9)
         RMFHT_SK(10) RMFHT_SK(11) RMFHT_SK(12) RMFHT_SK(13) RMFHT_SK(14)
