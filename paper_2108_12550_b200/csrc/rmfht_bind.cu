@@ -5,6 +5,7 @@
 #include "rmfht_fast.cuh"
 #include "rmfht_kernels.cuh"
 #include "rmfht_lane.cuh"
+#include "rmfht_pair.cuh"
 #include "rmfht_plan.h"
 
 #ifndef RMFHT_T
@@ -193,8 +194,62 @@ int prepare_lane(rmfht_plan* p) {
     return 0;
 }
 
+// pair kernel (rmfht_pair.cuh): p-FHT-FSCL, r = 2, L = 2, short codes
+template <int MM>
+int launch_pair(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint32_t* cw, void* pm, int32_t* att,
+                int32_t* path, void* att_pm, uint32_t* att_cw, long long B, void* /*work: none*/, cudaStream_t st) {
+    rmfht::Params<float> prm;
+    prm.llr = static_cast<const float*>(llr);
+    prm.maps = maps;
+    prm.B = B;
+    prm.M = p->M;
+    prm.perms = 1;
+    prm.tie_fix = 1;
+    prm.cw = cw;
+    prm.pm = static_cast<float*>(pm);
+    prm.attempt = att;
+    prm.path = path;
+    prm.att_pm = static_cast<float*>(att_pm);
+    prm.att_cw = att_cw;
+    if (B <= 0) return 0;
+    auto* mp = const_cast<rmfht_plan*>(p);
+    std::call_once(mp->once, [mp] { mp->prepared_rc = mp->prepare(mp); });
+    if (p->prepared_rc != 0) return p->prepared_rc;
+    const long long warps = (B * p->M + 15) / 16;
+    const long long blocks = (warps + 11) / 12;  // 12 lock-stepped warps per CTA, one CTA per SM
+    const long long grid = blocks < p->grid ? blocks : p->grid;
+    rmfht_pair::pair_kernel<MM><<<(unsigned)grid, 384, p->smem, st>>>(prm);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(RMFHT_ECUDA, std::string("pair kernel launch: ") + cudaGetErrorString(e));
+    return 0;
+}
+
+template <int MM>
+int prepare_pair(rmfht_plan* p) {
+    const size_t smem = (size_t)12 * (16 / p->M) * (1u << MM) * sizeof(float);
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rmfht_pair::pair_kernel<MM>, 384, smem);
+    if (e != cudaSuccess || per_sm < 1) return fail(RMFHT_ECUDA, "pair kernel does not fit an SM");
+    p->nwarps = 12;
+    p->smem = smem;
+    p->grid = sms * per_sm;
+    return 0;
+}
+
 template <typename T, int R, int MM, int L>
 int bind_one(rmfht_plan* p) {
+    if constexpr (sizeof(T) == 4 && R == 2 && L == 2 && MM >= 4 && MM <= 7) {
+        // p-FHT-FSCL, L = 2, short code, the M attempts of a frame within a
+        // warp's 16 items: two threads per item (RMFHT_NO_PAIR: A/B only)
+        if (p->fast && p->perms && 16 % p->M == 0 && !std::getenv("RMFHT_NO_PAIR")) {
+            p->pair = 1;
+            p->launch = &launch_pair<MM>;
+            p->prepare = &prepare_pair<MM>;
+            return 0;
+        }
+    }
     if constexpr (sizeof(T) == 4 && L == 1 && (1 << MM) <= 64 && (1 << MM) >= 4) {
         // FHT-FSC (L = 1, no permutations) on a short code: one thread per frame
         if (p->fast && !p->perms) {

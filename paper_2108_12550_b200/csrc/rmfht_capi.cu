@@ -330,10 +330,10 @@ int rmfht_plan_map_sizes(const rmfht_plan* p, int* sizes) {
 
 int rmfht_plan_record_u16(const rmfht_plan* p) { return p ? 2 * p->m + 2 : fail(RMFHT_EVALUE, "plan is NULL"); }
 
-int rmfht_plan_launches_per_call(const rmfht_plan* p) { return p ? (p->fast && !p->lane ? 2 : 1) : 0; }  // + 1 when sampled
+int rmfht_plan_launches_per_call(const rmfht_plan* p) { return p ? (p->fast && !p->lane && !p->pair ? 2 : 1) : 0; }  // + 1 when sampled
 
 int rmfht_plan_kernel(const rmfht_plan* p) {
-    return p ? (p->aut ? 4 : p->lane ? 5 : p->fast ? 2 : (p->generic ? 3 : 1)) : 0;
+    return p ? (p->aut ? 4 : p->lane ? 5 : p->pair ? 6 : p->fast ? 2 : (p->generic ? 3 : 1)) : 0;
 }
 
 int rmfht_expand_maps(const rmfht_plan* p, const uint16_t* raw, uint16_t* rec, long long count) {
