@@ -216,9 +216,10 @@ int launch_pair(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
     std::call_once(mp->once, [mp] { mp->prepared_rc = mp->prepare(mp); });
     if (p->prepared_rc != 0) return p->prepared_rc;
     const long long warps = (B * p->M + 15) / 16;
-    const long long blocks = (warps + 11) / 12;  // 12 lock-stepped warps per CTA, one CTA per SM
+    constexpr int PW = rmfht_pair::kPairWarps;  // lock-stepped warps per CTA, one CTA per SM
+    const long long blocks = (warps + PW - 1) / PW;
     const long long grid = blocks < p->grid ? blocks : p->grid;
-    rmfht_pair::pair_kernel<MM><<<(unsigned)grid, 384, p->smem, st>>>(prm);
+    rmfht_pair::pair_kernel<MM><<<(unsigned)grid, 32 * PW, p->smem, st>>>(prm);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(RMFHT_ECUDA, std::string("pair kernel launch: ") + cudaGetErrorString(e));
     return 0;
@@ -226,13 +227,14 @@ int launch_pair(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
 
 template <int MM>
 int prepare_pair(rmfht_plan* p) {
-    const size_t smem = (size_t)12 * (16 / p->M) * (1u << MM) * sizeof(float);
+    const size_t smem = (size_t)rmfht_pair::kPairWarps * (16 / p->M) * (1u << MM) * sizeof(float);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rmfht_pair::pair_kernel<MM>, 384, smem);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rmfht_pair::pair_kernel<MM>,
+                                                                  32 * rmfht_pair::kPairWarps, smem);
     if (e != cudaSuccess || per_sm < 1) return fail(RMFHT_ECUDA, "pair kernel does not fit an SM");
-    p->nwarps = 12;
+    p->nwarps = rmfht_pair::kPairWarps;
     p->smem = smem;
     p->grid = sms * per_sm;
     return 0;

@@ -37,6 +37,10 @@ using u32 = uint32_t;
 using u64 = unsigned long long;
 using rmfht::kFull;
 constexpr int L = 2;  // list size (paths per item)
+#ifndef RMFHT_PAIR_WARPS
+#define RMFHT_PAIR_WARPS 16  // lock-stepped warps per CTA (128 registers, one CTA per SM)
+#endif
+constexpr int kPairWarps = RMFHT_PAIR_WARPS;
 
 // |x| as an operand modifier.  It differs from the reference's x < 0 ? -x : x
 // only in the sign of a zero, which no comparison, sum or decision sees.
@@ -154,6 +158,23 @@ struct InvTab {
 template <int SS>
 using BitsT = typename std::conditional<(SS > 5), u64, u32>::type;
 
+// packed float32x2 (sm_100 FADD2): one instruction, two lanes of work (rmfht_fast.cuh)
+__device__ __forceinline__ u64 pk(float lo, float hi) {
+    return ((u64)__float_as_uint(hi) << 32) | (u64)__float_as_uint(lo);
+}
+__device__ __forceinline__ float plo(u64 v) { return __uint_as_float((u32)v); }
+__device__ __forceinline__ float phi(u64 v) { return __uint_as_float((u32)(v >> 32)); }
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+    u64 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+    u64 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
 // exchange with the partner thread (the other path of the item)
 template <typename X>
 __device__ __forceinline__ X other(X v) {
@@ -183,36 +204,42 @@ struct Node {  // per-thread list state of its path slot
 // fhtl with L = 2 (fht_decode.py:101-126): P = 2 paths, K = 2 bins each,
 // keep 2 of the pool of 4 by (pm, source, bin).  Returns this slot's
 // survivor codeword bits; *lin = its source slot.
+// (x is consumed: the transform runs in place)
 template <int SS>
-__device__ __forceinline__ BitsT<SS> fhtl2(const float (&x)[1 << SS], Node& nd, int q, int* lin) {
+__device__ __forceinline__ BitsT<SS> fhtl2(float (&x)[1 << SS], Node& nd, int q, int* lin) {
     constexpr int n = 1 << SS;
     const float llr = pw_sum<n>([&](int j) { return tabs(x[j]); });  // :114
-    float w[n];
+    float (&w)[n] = x;
+    // :28-48, two butterflies per packed f32x2 instruction (FADD2): pairs
+    // (lo, lo + half) and (lo + d, lo + half + d), d = 1 for half >= 2, else 2
 #pragma unroll
-    for (int k = 0; k < n; k++) w[k] = x[k];
-#pragma unroll
-    for (int t = 0; t < SS; t++) {  // :28-48
+    for (int t = 0; t < SS; t++) {
         const int half = n >> (t + 1);
+        const int d = half >= 2 ? 1 : 2;
 #pragma unroll
         for (int lo = 0; lo < n; lo++) {
-            if (lo & half) continue;
-            const float a = w[lo], b = w[lo + half];
-            w[lo] = b - a;
-            w[lo + half] = b + a;
+            if ((lo & half) || (lo & d)) continue;
+            const u64 a = pk(w[lo], w[lo + d]), b = pk(w[lo + half], w[lo + half + d]);
+            const u64 dd = sub2(b, a), ee = add2(b, a);
+            w[lo] = plo(dd);
+            w[lo + d] = phi(dd);
+            w[lo + half] = plo(ee);
+            w[lo + half + d] = phi(ee);
         }
     }
     // top-2 bins by |w| descending, ties to the lower bin (:116)
     float a1 = -1.f, a2 = -1.f, w1 = 0.f, w2 = 0.f;
     int b1 = 0, b2 = 1;
 #pragma unroll
-    for (int k = 0; k < n; k++) {
+    for (int k = 0; k < n; k++) {  // branch-free (selects)
         const float a = tabs(w[k]);
-        if (a > a1) {
-            a2 = a1; w2 = w1; b2 = b1;
-            a1 = a; w1 = w[k]; b1 = k;
-        } else if (a > a2) {
-            a2 = a; w2 = w[k]; b2 = k;
-        }
+        const bool g1 = a > a1, g2 = a > a2;
+        a2 = g1 ? a1 : (g2 ? a : a2);
+        w2 = g1 ? w1 : (g2 ? w[k] : w2);
+        b2 = g1 ? b1 : (g2 ? k : b2);
+        a1 = g1 ? a : a1;
+        w1 = g1 ? w[k] : w1;
+        b1 = g1 ? k : b1;
     }
     // pool (:119-120): candidate c = slot * 2 + k
     float cpm[4], cw[4];
@@ -367,7 +394,7 @@ __device__ __forceinline__ BitsT<SS> spc2(const float (&x)[1 << SS], Node& nd, i
 
 // _decode_node without permutations (RR >= 2, below the root)
 template <int RR, int SS>
-__device__ __forceinline__ BitsT<SS> node(const float (&x)[1 << SS], Node& nd, int q, int* lin) {
+__device__ __forceinline__ BitsT<SS> node(float (&x)[1 << SS], Node& nd, int q, int* lin) {
     constexpr int n = 1 << SS, h = n / 2;
     if constexpr (RR == 1) {
         return fhtl2<SS>(x, nd, q, lin);
@@ -406,7 +433,7 @@ struct Out2 {  // root-domain bits of a path, N = 2^MM <= 128
 };
 
 template <int MM>
-__global__ void __launch_bounds__(384, 1) pair_kernel(rmfht::Params<float> prm) {
+__global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<float> prm) {
     constexpr int N = 1 << MM, H = N / 2, NW = N >= 32 ? N / 32 : 1, S = L + 2 * L;
     static_assert(MM >= 4 && MM <= 7, "pair kernel: RM(2, m), 4 <= m <= 7");
     constexpr int REC = 2 * MM + 2;
@@ -454,12 +481,22 @@ __global__ void __launch_bounds__(384, 1) pair_kernel(rmfht::Params<float> prm) 
         InvTab<MM> tb0, tb1;
         tb0.build(c0);
         tb1.build(c1);
-        float lm0 = pw_sum<H>([&](int j) {
-            return fminf(fabsf(alpha[tb0.at(j)]), fabsf(alpha[tb0.at(j + H)]));
-        });
-        float lm1 = pw_sum<H>([&](int j) {
-            return fminf(fabsf(alpha[tb1.at(j)]), fabsf(alpha[tb1.at(j + H)]));
-        });
+        float lmv[2];
+#pragma unroll 1
+        for (int tt = 0; tt < 2; tt++) {  // one copy of the 64-pair body (instruction cache)
+            InvTab<MM> tb;
+#pragma unroll
+            for (int v = 0; v < InvTab<MM>::NA; v++) tb.A[v] = tt ? tb1.A[v] : tb0.A[v];
+#pragma unroll
+            for (int v = 0; v < InvTab<MM>::NB; v++) tb.B[v] = tt ? tb1.B[v] : tb0.B[v];
+            tb.top = tt ? tb1.top : tb0.top;
+            const float v = pw_sum<H>([&](int j) {
+                return fminf(fabsf(alpha[tb.at(j)]), fabsf(alpha[tb.at(j + H)]));
+            });
+            if (tt) lmv[1] = v;
+            else lmv[0] = v;
+        }
+        const float lm0 = lmv[0], lm1 = lmv[1];
         // all four trials: t = 0 (slot 0), 1 (slot 1), 2 (slot 0), 3 (slot 1)
         float lm[4];
         u32 key[4];
@@ -557,25 +594,50 @@ __global__ void __launch_bounds__(384, 1) pair_kernel(rmfht::Params<float> prm) 
         Out2<MM> bb;
 #pragma unroll
         for (int w = 0; w < (N > 64 ? 2 : 1); w++) bb.w[w] = from_slot(ob.w[w], q, best);
-        u32 cw[NW];
+        // sigma(32 t + i) = (b ^ A 32t) ^ (A i): per-word base, tables over i
+        constexpr int PB = N < 32 ? MM : 5;  // bits of i within a word
+        u32 tlo[8], thi[PB > 3 ? 1 << (PB - 3) : 1];
 #pragma unroll
-        for (int t = 0; t < NW; t++) {
+        for (int v = 0; v < 8; v++) {
+            u32 e = 0;
+#pragma unroll
+            for (int k = 0; k < 3 && k < PB; k++) e ^= ((v >> k) & 1) ? cf.col[k] : 0u;
+            tlo[v] = e;
+        }
+#pragma unroll
+        for (int v = 0; v < (PB > 3 ? 1 << (PB - 3) : 1); v++) {
+            u32 e = 0;
+#pragma unroll
+            for (int k = 3; k < PB; k++) e ^= ((v >> (k - 3)) & 1) ? cf.col[k] : 0u;
+            thi[v] = e;
+        }
+        constexpr int WPT = NW > 1 ? NW / 2 : 1;  // words per thread: t = 2 j + q
+        u32 mine[WPT];
+#pragma unroll
+        for (int j = 0; j < WPT; j++) {
+            const int t = NW > 1 ? 2 * j + q : 0;
+            const u32 base = cf.fwd((u32)(t * 32));
             u32 word = 0;
-            if (t % 2 == q || NW == 1) {
 #pragma unroll
-                for (int i = 0; i < (N < 32 ? N : 32); i++) {
-                    const u32 e = cf.fwd((u32)(t * 32 + i));
-                    const u32 bit = (u32)((bb.w[e >> 6] >> (e & 63)) & 1ull);
-                    word |= bit << i;
-                }
+            for (int i = 0; i < (N < 32 ? N : 32); i++) {
+                const u32 e = base ^ tlo[i & 7] ^ thi[(i >> 3) & ((PB > 3 ? 1 << (PB - 3) : 1) - 1)];
+                u64 src = bb.w[0];
+                if constexpr (N > 64) src = (e & 64) ? bb.w[1] : bb.w[0];
+                word |= (u32)((src >> (e & 63)) & 1ull) << i;
             }
-            cw[t] = word;
+            mine[j] = word;
         }
         // exchange halves: both threads of the item hold the whole codeword
+        u32 cw[NW];
 #pragma unroll
-        for (int t = 0; t < NW; t++) {
-            const u32 o = other(cw[t]);
-            if (NW > 1 && t % 2 != q) cw[t] = o;
+        for (int j = 0; j < WPT; j++) {
+            const u32 o = other(mine[j]);
+            if (NW > 1) {
+                cw[2 * j] = q == 0 ? mine[j] : o;
+                cw[2 * j + 1] = q == 0 ? o : mine[j];
+            } else {
+                cw[0] = mine[0];
+            }
         }
         // reported pm of this attempt (rmfht::CorrPm order: "lane" l sums
         // positions l + 32 t in double, then the xor tree 16 .. 1)
@@ -607,13 +669,12 @@ __global__ void __launch_bounds__(384, 1) pair_kernel(rmfht::Params<float> prm) 
                 for (int l = 0; l < off; l++) qv[l] = qv[l] + qv[l + off];
             return (float)qv[0];
         };
-        if (prm.att_pm || prm.att_cw) {
-            const float rep = corr();
-            if (live && q == 0) {
-                if (prm.att_pm) prm.att_pm[item] = rep;
-                if (prm.att_cw)
-                    for (int t = 0; t < NW; t++) prm.att_cw[item * NW + t] = cw[t];
-            }
+        // every attempt's reported pm (one inlined copy: the winners' come from it)
+        const float rep = corr();
+        if (live && q == 0) {
+            if (prm.att_pm) prm.att_pm[item] = rep;
+            if (prm.att_cw)
+                for (int t = 0; t < NW; t++) prm.att_cw[item * NW + t] = cw[t];
         }
         // ensemble pick over the frame's M attempts (items it - at .. + M - 1):
         // first strict minimum of the accumulated pm (top_decoders.py:200)
@@ -627,9 +688,6 @@ __global__ void __launch_bounds__(384, 1) pair_kernel(rmfht::Params<float> prm) 
             if (opv < vpm || (opv == vpm && oat < vat)) { vpm = opv; vat = oat; }
         }
         const bool winner = live && vat == at;
-        // the winner's reported pm (warp-uniform branch on any winner)
-        float rep = 0.f;
-        if (__any_sync(kFull, winner)) rep = corr();
         if (winner && q == 0) {
             for (int t = 0; t < NW; t++) prm.cw[fidx * NW + t] = cw[t];
             prm.pm[fidx] = rep;

@@ -43,3 +43,36 @@ def test_lane_kernel_exact_ties_fixture():
     o = plan.decode(g["llr"])
     assert np.array_equal(o["cw"], g["cw_bits"])
     assert np.array_equal(o["pm"].astype(np.float64), g["pm"])
+
+
+# ---------------------------------------------------------------- pair kernel
+@pytest.mark.parametrize("m,M", [(7, 4), (7, 1), (7, 2), (7, 8), (7, 16), (4, 4)])
+def test_pair_kernel_matches_reference_order_kernel(m, M, oracle_mod):
+    """Pair kernel (plan kernel 6: r = 2, L = 2, two threads per item) vs the
+    reference-order float32 kernel and the float32 oracle (order
+    "reference"): every output bit-exact, every attempt's pm and codeword
+    included; M not dividing 16 binds the warp-per-item kernel instead."""
+    from paper_2108_12550_b200.channel_model import synthetic_frames
+    from paper_2108_12550_b200.decoder import Plan
+    from paper_2108_12550_b200.rm_core import build_code
+    spec = build_code(2, m)
+    B = 1000 + 37
+    _, llr = synthetic_frames(spec, 1.5, B, seed=m * 31 + M)
+    plan = Plan(2, m, 2, M, True, "f32")
+    assert plan.kernel == 6
+    ref = Plan(2, m, 2, M, True, "f32", reference_order=True)
+    assert ref.kernel == 1
+    raw, rec = plan.sample(B, seed=9 + M)
+    a = plan.decode(llr, records=rec, diag=True)
+    b = ref.decode(llr, records=rec, diag=True)
+    for k in ("cw", "pm", "attempt", "path", "att_pm", "att_cw"):
+        assert np.array_equal(a[k], b[k]), k
+    c = oracle_mod.decode(2, m, 2, M, llr, raw, dtype=np.float32, nthreads=16)
+    assert np.array_equal(a["cw"], c["cw"]) and np.array_equal(a["pm"], c["pm"])
+    assert np.array_equal(a["attempt"], c["attempt"])
+
+
+def test_pair_kernel_not_for_m_not_dividing_16():
+    from paper_2108_12550_b200.decoder import Plan
+    assert Plan(2, 7, 2, 3, True, "f32").kernel == 2
+    assert Plan(2, 7, 2, 4, True, "f64").kernel == 1
