@@ -204,7 +204,7 @@ int launch_pair(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
     prm.B = B;
     prm.M = p->M;
     prm.perms = 1;
-    prm.tie_fix = 1;
+    prm.tie_fix = p->tie_fix;
     prm.cw = cw;
     prm.pm = static_cast<float*>(pm);
     prm.attempt = att;

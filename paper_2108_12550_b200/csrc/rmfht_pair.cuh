@@ -507,9 +507,10 @@ __global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<
             lm[q] = lm0; lm[q + 2] = lm1; lm[1 - q] = o0; lm[3 - q] = o1;
             key[q] = k0; key[q + 2] = k1; key[1 - q] = ok0; key[3 - q] = ok1;
         }
-        // tie fix: equal pairing directions keep equal LM (select_trials)
+        // tie fix: equal pairing directions keep equal LM (select_trials;
+        // on by default for float32, RMFHT_NO_TIE_FIX turns it off)
 #pragma unroll
-        for (int t = 1; t < 4; t++) {
+        for (int t = 1; t < 4 && prm.tie_fix; t++) {
             bool done = false;
 #pragma unroll
             for (int s = 0; s < t; s++)

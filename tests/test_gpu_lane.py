@@ -76,3 +76,21 @@ def test_pair_kernel_not_for_m_not_dividing_16():
     from paper_2108_12550_b200.decoder import Plan
     assert Plan(2, 7, 2, 3, True, "f32").kernel == 2
     assert Plan(2, 7, 2, 4, True, "f64").kernel == 1
+
+
+def test_pair_kernel_honours_no_tie_fix(oracle_mod):
+    """tie_fix=False (RMFHT_NO_TIE_FIX) on the pair kernel equals the
+    reference-order kernel and the oracle without the tie fix."""
+    from paper_2108_12550_b200.channel_model import synthetic_frames
+    from paper_2108_12550_b200.decoder import Plan
+    from paper_2108_12550_b200.rm_core import build_code
+    _, llr = synthetic_frames(build_code(2, 7), 2.0, 800, seed=5)
+    a_plan = Plan(2, 7, 2, 4, True, "f32", tie_fix=False)
+    assert a_plan.kernel == 6
+    raw, rec = a_plan.sample(800, seed=3)
+    a = a_plan.decode(llr, records=rec, diag=True)
+    b = Plan(2, 7, 2, 4, True, "f32", tie_fix=False, reference_order=True).decode(llr, records=rec, diag=True)
+    for k in ("cw", "pm", "attempt", "att_pm"):
+        assert np.array_equal(a[k], b[k]), k
+    c = oracle_mod.decode(2, 7, 2, 4, llr, raw, dtype=np.float32, tie_fix=False, nthreads=16)
+    assert np.array_equal(a["cw"], c["cw"]) and np.array_equal(a["pm"], c["pm"])
