@@ -227,7 +227,8 @@ int launch_pair(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
 
 template <int MM>
 int prepare_pair(rmfht_plan* p) {
-    const size_t smem = (size_t)rmfht_pair::kPairWarps * (16 / p->M) * (1u << MM) * sizeof(float);
+    const size_t smem = (size_t)rmfht_pair::kPairWarps * (16 / p->M) * (1u << MM) * sizeof(float) +
+                        (size_t)(4u << MM);  // alignment pad of the frame buffers
     cudaError_t a = cudaFuncSetAttribute(rmfht_pair::pair_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (a != cudaSuccess) return fail(RMFHT_ECUDA, std::string("pair smem attribute: ") + cudaGetErrorString(a));

@@ -153,7 +153,22 @@ struct InvTab {
         const u32 v = A[j % NA] ^ B[(j / NA) % NB];
         return ((j >> (MM - 1)) & 1) ? v ^ top : v;
     }
+    // the same as byte offsets OR-ed into a shared-window base aligned to 4N
+    // bytes: one LOP3 per gather address (rmfht_fast.cuh RootIdx)
+    __device__ __forceinline__ void rebase(u32 base) {
+#pragma unroll
+        for (int q = 0; q < NA; q++) A[q] = base | (A[q] << 2);
+#pragma unroll
+        for (int q = 0; q < NB; q++) B[q] <<= 2;
+        top <<= 2;
+    }
 };
+
+__device__ __forceinline__ float lds(u32 saddr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(saddr));
+    return v;
+}
 
 template <int SS>
 using BitsT = typename std::conditional<(SS > 5), u64, u32>::type;
@@ -437,7 +452,10 @@ __global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<
     constexpr int N = 1 << MM, H = N / 2, NW = N >= 32 ? N / 32 : 1, S = L + 2 * L;
     static_assert(MM >= 4 && MM <= 7, "pair kernel: RM(2, m), 4 <= m <= 7");
     constexpr int REC = 2 * MM + 2;
-    extern __shared__ __align__(16) float fr[];  // per warp: the frames of its 16 items
+    extern __shared__ __align__(16) unsigned char fraw[];  // per warp: the frames of its 16 items
+    // frames start 4N-byte aligned in the shared window (gather offsets are OR-ed in)
+    const u32 rs = (u32)__cvta_generic_to_shared(fraw);
+    float* const fr = reinterpret_cast<float*>(fraw + ((((rs + 4 * N - 1) / (4 * N)) * (4 * N)) - rs));
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int M = prm.M, FPW = 16 / M;  // frames per warp (M divides 16)
     float* fw = fr + (size_t)wib * FPW * N;
@@ -470,6 +488,7 @@ __global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<
         const long long fidx = live ? item / M : f0;
         const int at = live ? (int)(item - fidx * M) : 0;
         const float* alpha = fw + (fidx - f0) * N;
+        const u32 abase = (u32)__cvta_generic_to_shared(alpha);
         // this thread's maps: root map q, trial maps q and q + 2 (both permute path q)
         const uint16_t* rec = prm.maps + (size_t)(live ? item : item0) * S * REC;
         Map<MM> root, t0, t1;
@@ -481,6 +500,8 @@ __global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<
         InvTab<MM> tb0, tb1;
         tb0.build(c0);
         tb1.build(c1);
+        tb0.rebase(abase);
+        tb1.rebase(abase);
         float lmv[2];
 #pragma unroll 1
         for (int tt = 0; tt < 2; tt++) {  // one copy of the 64-pair body (instruction cache)
@@ -491,7 +512,7 @@ __global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<
             for (int v = 0; v < InvTab<MM>::NB; v++) tb.B[v] = tt ? tb1.B[v] : tb0.B[v];
             tb.top = tt ? tb1.top : tb0.top;
             const float v = pw_sum<H>([&](int j) {
-                return fminf(fabsf(alpha[tb.at(j)]), fabsf(alpha[tb.at(j + H)]));
+                return fminf(fabsf(lds(tb.at(j))), fabsf(lds(tb.at(j + H))));
             });
             if (tt) lmv[1] = v;
             else lmv[0] = v;
@@ -548,9 +569,10 @@ __global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<
         // ---- root: f from the frame through my composite (:100)
         InvTab<MM> tc;
         tc.build(comp);
+        tc.rebase(abase);
         float xl[H];
 #pragma unroll
-        for (int j = 0; j < H; j++) xl[j] = f_op(alpha[tc.at(j)], alpha[tc.at(j + H)]);
+        for (int j = 0; j < H; j++) xl[j] = f_op(lds(tc.at(j)), lds(tc.at(j + H)));
         int l1;
         const BitsT<MM - 1> bl = node<1, MM - 1>(xl, nd, q, &l1);  // :101 (RM(1, m-1): FHT)
         // g through the composite of slot l1 (:102-104)
@@ -561,10 +583,11 @@ __global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<
             for (int k = 0; k < MM; k++) cs.icol[k] = from_slot(comp.icol[k], q, l1);
             cs.c = from_slot(comp.c, q, l1);
             tg.build(cs);
+            tg.rebase(abase);
         }
         float xr[H];
 #pragma unroll
-        for (int j = 0; j < H; j++) xr[j] = g_op(alpha[tg.at(j)], alpha[tg.at(j + H)], (int)((bl >> j) & 1));
+        for (int j = 0; j < H; j++) xr[j] = g_op(lds(tg.at(j)), lds(tg.at(j + H)), (int)((bl >> j) & 1));
         int l2;
         const BitsT<MM - 1> br = node<2, MM - 1>(xr, nd, q, &l2);  // :105
         const BitsT<MM - 1> blm = from_slot(bl, q, l2);
