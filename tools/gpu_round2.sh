@@ -19,7 +19,7 @@ cap() {  # config kernel-regex frames
     python bench.py --steps 1 --warmup 3 --no-cpu --config $1 --frames $3 > $o/${tag}_ncu_$1.log 2>&1; echo ncu $1 $?
 }
 cap rm29_L4_M20 decode_kernel2 16384
-cap rm27_L2_M4 decode_kernel2 65536
+cap rm27_L2_M4 pair_kernel 65536
 cap rm37_L8_M32 decode_kernel2 8192
 cap rm29_L1_M512 decode_kernel2 512
 cap rm25_fhtfsc lane_kernel 1048576
