@@ -1618,7 +1618,10 @@ __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Par
     // the launch always uses fast_warps() warps (prepare_fast): a compile-time
     // count keeps the per-warp scratch addresses cheap to rematerialise
     constexpr int nwarps = fast_warps<R, MM, L>();
-    const int warp = threadIdx.x >> 5, lane = lane_id();
+    // (warp index through a shuffle: provably warp-uniform, so the per-warp
+    // scratch addresses live in uniform registers instead of being
+    // rematerialised from threadIdx under register pressure)
+    const int warp = __shfl_sync(kFull, (int)(threadIdx.x >> 5), 0), lane = lane_id();
     // per-warp frame LLRs, each 2 KB aligned in the shared window, then the scratch
     const u32 raw_saddr = (u32)__cvta_generic_to_shared(smem_raw);
     const u32 pad = ((raw_saddr + 2047u) & ~2047u) - raw_saddr;
