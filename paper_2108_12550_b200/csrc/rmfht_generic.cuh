@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(128) decode_kernel_generic(rmfht::Params<T> pr
     const int N = sh.N, L = sh.L, MM = sh.m, NW = N / 32 > 0 ? N / 32 : 1, REC = 2 * MM + 2;
     T* alpha = reinterpret_cast<T*>(smem_raw);
     unsigned char* wbase = smem_raw + ((N * sizeof(T) + 15) / 16) * 16;
-    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = lane_id();
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), nwarps = blockDim.x >> 5, lane = lane_id();  // provably warp-uniform
     unsigned char* mine = wbase + (size_t)warp * lay.total;
     W<T> w;
     w.lvl = reinterpret_cast<T*>(mine + lay.lvl);

@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(256) decode_kernel(Params<T> prm) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* alpha = reinterpret_cast<T*>(smem_raw);
     WS* wsarr = reinterpret_cast<WS*>(smem_raw + ((N * sizeof(T) + 15) / 16) * 16);
-    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = lane_id();
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), nwarps = blockDim.x >> 5, lane = lane_id();  // provably warp-uniform
     WS& ws = wsarr[warp];
     Ctx<T, R, MM, L> cx{ws, alpha, prm.perms, prm.tie_fix};
     const int Meff = prm.perms ? prm.M : 1;

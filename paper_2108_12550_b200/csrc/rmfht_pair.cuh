@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<
     // frames start 4N-byte aligned in the shared window (gather offsets are OR-ed in)
     const u32 rs = (u32)__cvta_generic_to_shared(fraw);
     float* const fr = reinterpret_cast<float*>(fraw + ((((rs + 4 * N - 1) / (4 * N)) * (4 * N)) - rs));
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, wib = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // provably warp-uniform
     const int M = prm.M, FPW = 16 / M;  // frames per warp (M divides 16)
     float* fw = fr + (size_t)wib * FPW * N;
     const int q = lane & 1, it = lane >> 1;
