@@ -757,6 +757,10 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
         }
         __syncwarp();
     } else {
+#ifdef RMFHT_STATS
+    if (__all_sync(kFull, cnt <= 1)) RMFHT_STAT(100 + SS);  // no lane holds two candidates
+    if (__all_sync(kFull, cnt <= 2)) RMFHT_STAT(110 + SS);
+#endif
     if constexpr (LAZY) spill();
     // General case, more than 32 candidates: L rounds of warp-wide minimum
     // selection over the pool key (pm, source path, bin) (:120), each lane

@@ -55,7 +55,8 @@ for ss in range(3, 9):
     if n:
         print(f"FHT 2^{ss}: {n / items:.2f}/item  common {common / n:.3f}  greedy {greedy / n:.3f} "
               f"(collision -> exact list {exact / n:.3f}; over {over / n:.3f})  fallback {fb / n:.4f}  "
-              f"mean cand {tot / n:.1f}")
+              f"mean cand {tot / n:.1f}  off-common with every lane <= 1 cand {int(st[100 + ss]) / max(1, n - common):.3f}"
+              f"  <= 2 cand {int(st[110 + ss]) / max(1, n - common):.3f}")
 cnt, s1, s2, mx = int(st[202]), int(st[200]), int(st[201]) * 1024, int(st[203])
 if cnt:
     mean = s1 / cnt
