@@ -1627,12 +1627,14 @@ __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Par
     // rematerialised from threadIdx under register pressure)
     const int warp = __shfl_sync(kFull, (int)(threadIdx.x >> 5), 0), lane = lane_id();
     // per-warp frame LLRs, each 2 KB aligned in the shared window, then the scratch
-    const u32 raw_saddr = (u32)__cvta_generic_to_shared(smem_raw);
+    // (the scratch first: its addresses need no alignment arithmetic; the
+    // compiler rematerialises them all over the kernel)
+    static_assert(sizeof(WS) % 16 == 0, "scratch stride");
+    WS& ws = reinterpret_cast<WS*>(smem_raw)[warp];
+    const u32 raw_saddr = (u32)__cvta_generic_to_shared(smem_raw) + (u32)(nwarps * sizeof(WS));
     const u32 pad = ((raw_saddr + 2047u) & ~2047u) - raw_saddr;
     constexpr u32 ASTRIDE = (u32)N * 4u;  // N-aligned: gather offsets (< 4N bytes) are OR-ed into the base
-    float* const alpha_w = reinterpret_cast<float*>(smem_raw + pad + (size_t)warp * ASTRIDE);
-    WS* wsarr = reinterpret_cast<WS*>(smem_raw + pad + (size_t)nwarps * ASTRIDE);
-    WS& ws = wsarr[warp];
+    float* const alpha_w = reinterpret_cast<float*>(smem_raw + nwarps * sizeof(WS) + pad + (size_t)warp * ASTRIDE);
     const u32 asa = (u32)__cvta_generic_to_shared(alpha_w);
     Ctx2<R, MM, L> cx{ws, alpha_w, nullptr, PM ? 1 : 0, {}, lane, lane / C::LPP, lane % C::LPP, asa};
     static_assert(sizeof(MapR<MM>) == 2 * (2 * MM + 2), "record layout");
