@@ -159,8 +159,10 @@ int rmfht_plan_launches_per_call(const rmfht_plan *plan);
 /* Which kernel the plan runs: 1 = reference-order (rmfht_kernels.cuh),
  * 2 = float32 throughput kernel (rmfht_fast.cuh), 3 = generic runtime-shaped
  * kernel (rmfht_generic.cuh, reference order), 4 = Aut-SSC (rmfht_ssc.cu),
- * 5 = lane-per-frame FHT-FSC kernel for N <= 64 (rmfht_lane.cuh);
- * 0 for a NULL plan. */
+ * 5 = lane-per-frame FHT-FSC kernel for N <= 64 (rmfht_lane.cuh),
+ * 6 = pair kernel, r = 2, L = 2, N <= 128 (rmfht_pair.cuh),
+ * 7 = lane-group kernel, r = 2, L = 1, m = 8 or 9, M a multiple of 4
+ * (rmfht_grp.cuh); 0 for a NULL plan. */
 int rmfht_plan_kernel(const rmfht_plan *plan);
 
 const char *rmfht_last_error(void);

@@ -3,6 +3,7 @@
 #include <cstdlib>
 
 #include "rmfht_fast.cuh"
+#include "rmfht_grp.cuh"
 #include "rmfht_kernels.cuh"
 #include "rmfht_lane.cuh"
 #include "rmfht_pair.cuh"
@@ -244,8 +245,87 @@ int prepare_pair(rmfht_plan* p) {
     return 0;
 }
 
+// lane-group kernel (rmfht_grp.cuh): p-FHT-FSCL, r = 2, L = 1, four attempts of a frame per warp
+template <int MM>
+int launch_grp(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint32_t* cw, void* pm, int32_t* att,
+               int32_t* path, void* att_pm, uint32_t* att_cw, long long B, void* work, cudaStream_t st) {
+    rmfht::Params<float> prm;
+    prm.llr = static_cast<const float*>(llr);
+    prm.maps = maps;
+    prm.B = B;
+    prm.M = p->M;
+    prm.perms = 1;
+    prm.tie_fix = (p->lockstep & 0xff) << 8;
+    prm.cw = cw;
+    prm.pm = static_cast<float*>(pm);
+    prm.attempt = att;
+    prm.path = path;
+    prm.att_pm = static_cast<float*>(att_pm);
+    prm.att_cw = att_cw;
+    if (B <= 0) return 0;
+    auto* mp = const_cast<rmfht_plan*>(p);
+    std::call_once(mp->once, [mp] { mp->prepared_rc = mp->prepare(mp); });
+    if (p->prepared_rc != 0) return p->prepared_rc;
+    // frame chunks as launch_fast (32-bit item counts in the reduce kernel's grid)
+    const long long chunk = rmfht_chunk_frames(p);
+    constexpr int N = 1 << MM, NW = N / 32, S = rmfht_grp::kMaps, REC = 2 * MM + 2;
+    constexpr int PW = rmfht_grp::kGrpWarps;
+    for (long long f0 = 0; f0 < B; f0 += chunk) {
+        const long long Bc = B - f0 < chunk ? B - f0 : chunk;
+        rmfht::Params<float> q = prm;
+        q.B = Bc;
+        q.llr = prm.llr + f0 * N;
+        q.maps = prm.maps + (size_t)f0 * p->M * S * REC;
+        q.cw = prm.cw + f0 * NW;
+        q.pm = prm.pm + f0;
+        q.attempt = prm.attempt + f0;
+        q.path = prm.path + f0;
+        if (prm.att_pm) q.att_pm = prm.att_pm + f0 * p->M;
+        if (prm.att_cw) q.att_cw = prm.att_cw + (size_t)f0 * p->M * NW;
+        const size_t items = (size_t)Bc * p->M;
+        auto* hdr = static_cast<rmfht2::AttHdr*>(work);
+        auto* bits = reinterpret_cast<unsigned long long*>(static_cast<char*>(work) + items * sizeof(rmfht2::AttHdr));
+        const long long rounds = (long long)items / rmfht_grp::kItems;
+        const long long blocks_needed = (rounds + PW - 1) / PW;
+        const long long grid = blocks_needed < p->grid ? blocks_needed : p->grid;
+        rmfht_grp::grp_kernel<MM><<<(unsigned)grid, 32 * PW, p->smem, st>>>(q, hdr, bits);
+        rmfht2::reduce_kernel2<2, MM, 1, rmfht_grp::kLpp><<<(unsigned)((Bc + 7) / 8), 256, 0, st>>>(q, hdr, bits);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(RMFHT_ECUDA, std::string("lane-group kernel launch: ") + cudaGetErrorString(e));
+    return 0;
+}
+
+template <int MM>
+int prepare_grp(rmfht_plan* p) {
+    const size_t smem = rmfht_grp::smem_bytes<MM>(rmfht_grp::kGrpWarps);
+    auto kern = rmfht_grp::grp_kernel<MM>;
+    cudaError_t a = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (a != cudaSuccess) return fail(RMFHT_ECUDA, std::string("lane-group smem attribute: ") + cudaGetErrorString(a));
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * rmfht_grp::kGrpWarps, smem);
+    if (e != cudaSuccess || per_sm < 1) return fail(RMFHT_ECUDA, "lane-group kernel does not fit an SM");
+    p->nwarps = rmfht_grp::kGrpWarps;
+    p->smem = smem;
+    p->grid = sms * per_sm;
+    return 0;
+}
+
 template <typename T, int R, int MM, int L>
 int bind_one(rmfht_plan* p) {
+    if constexpr (sizeof(T) == 4 && R == 2 && L == 1 && MM >= 8 && MM <= 9) {
+        // p-FHT-FSCL with one path: four attempts of a frame per warp
+        // (RMFHT_NO_GRP: A/B and cross-check against the throughput kernel)
+        if (p->fast && p->perms && p->M % rmfht_grp::kItems == 0 && !std::getenv("RMFHT_NO_GRP")) {
+            p->grp = 1;
+            p->work_per_item = rmfht_grp::work_bytes();
+            p->launch = &launch_grp<MM>;
+            p->prepare = &prepare_grp<MM>;
+            return 0;
+        }
+    }
     if constexpr (sizeof(T) == 4 && R == 2 && L == 2 && MM >= 4 && MM <= 7) {
         // p-FHT-FSCL, L = 2, short code, the M attempts of a frame within a
         // warp's 16 items: two threads per item (RMFHT_NO_PAIR: A/B only)

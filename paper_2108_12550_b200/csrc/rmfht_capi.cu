@@ -333,7 +333,7 @@ int rmfht_plan_record_u16(const rmfht_plan* p) { return p ? 2 * p->m + 2 : fail(
 int rmfht_plan_launches_per_call(const rmfht_plan* p) { return p ? (p->fast && !p->lane && !p->pair ? 2 : 1) : 0; }  // + 1 when sampled
 
 int rmfht_plan_kernel(const rmfht_plan* p) {
-    return p ? (p->aut ? 4 : p->lane ? 5 : p->pair ? 6 : p->fast ? 2 : (p->generic ? 3 : 1)) : 0;
+    return p ? (p->aut ? 4 : p->lane ? 5 : p->pair ? 6 : p->grp ? 7 : p->fast ? 2 : (p->generic ? 3 : 1)) : 0;
 }
 
 int rmfht_expand_maps(const rmfht_plan* p, const uint16_t* raw, uint16_t* rec, long long count) {

@@ -1759,10 +1759,13 @@ __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Par
 // Per frame: first strict minimum over attempts (top_decoders.py:200), then
 // un-permute the winner's root-domain bits by its composite root map
 // (:147-150): codeword bit i = beta[sigma(i)], sigma = trial o init.
-template <int R, int MM, int L>
+// LPPX: lanes per path of the kernel that wrote the records (bit k of lane
+// u's word = element k * LPPX + u); the lane-group kernel (rmfht_grp.cuh)
+// writes 8-lane records for L = 1
+template <int R, int MM, int L, int LPPX = Cfg<R, MM, L>::LPP>
 __global__ void __launch_bounds__(256) reduce_kernel2(rmfht::Params<float> prm, const AttHdr* hdr, const u64* bitsin) {
     using C = Cfg<R, MM, L>;
-    constexpr int N = C::N, NW = N / 32, S = C::S, REC = 2 * MM + 2, LPP = C::LPP;
+    constexpr int N = C::N, NW = N / 32, S = C::S, REC = 2 * MM + 2, LPP = LPPX;
     __shared__ u64 sbits[8][LPP];
     __shared__ MapS smap[8];
     const int warp = threadIdx.x >> 5, lane = lane_id();

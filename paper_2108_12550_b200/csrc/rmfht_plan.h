@@ -22,6 +22,7 @@ struct rmfht_plan {
     int generic = 0;  // runtime-shaped interpreter kernel (rmfht_generic.cuh)
     int lane = 0;     // lane-per-frame kernel (rmfht_lane.cuh): FHT-FSC on N <= 64
     int pair = 0;     // pair kernel (rmfht_pair.cuh): r = 2, L = 2, N <= 128
+    int grp = 0;      // lane-group kernel (rmfht_grp.cuh): r = 2, L = 1, m = 8, 9, M % 4 == 0
     int force_generic = 0;
     int aut = 0;  // Aut-SSC plan (RMFHT_AUT_SSC): M = P single-map SSC decodes per frame
     int S, nwarps, grid;

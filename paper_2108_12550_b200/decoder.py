@@ -87,7 +87,7 @@ class Plan:
         self.rec_u16 = lib.rmfht_plan_record_u16(h)
         self.words = max(1, self.N // 32)
         self.launches_per_call = lib.rmfht_plan_launches_per_call(h)
-        self.kernel = lib.rmfht_plan_kernel(h)  # 1 reference-order, 2 float32 throughput, 3 generic, 4 Aut-SSC, 5 lane, 6 pair
+        self.kernel = lib.rmfht_plan_kernel(h)  # 1 reference-order, 2 float32 throughput, 3 generic, 4 Aut-SSC, 5 lane, 6 pair, 7 lane-group
 
     def __del__(self):
         h = getattr(self, "_h", None)
