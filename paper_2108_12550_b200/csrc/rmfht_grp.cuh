@@ -52,7 +52,7 @@ constexpr int kItems = 4;  // items per warp
 constexpr int kMaps = 3;   // maps per attempt: the root map and two trials (r = 2, L = 1)
 
 #ifndef RMFHT_GRP_WARPS
-#define RMFHT_GRP_WARPS 16
+#define RMFHT_GRP_WARPS 24
 #endif
 constexpr int kGrpWarps = RMFHT_GRP_WARPS;
 
