@@ -21,6 +21,6 @@ cap() {  # config kernel-regex frames
 cap rm29_L4_M20 decode_kernel2 16384
 cap rm27_L2_M4 pair_kernel 65536
 cap rm37_L8_M32 decode_kernel2 8192
-cap rm29_L1_M512 decode_kernel2 512
+cap rm29_L1_M512 grp_kernel 1024
 cap rm25_fhtfsc lane_kernel 1048576
 cap rm29_autssc_P512 aut_ssc 1024
