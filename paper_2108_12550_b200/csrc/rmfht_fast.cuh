@@ -1748,9 +1748,11 @@ __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Par
         }
         // lock-step rounds: warps share the instruction stream (named barrier per group)
         const int grp = (prm.tie_fix >> 8) & 0xff;  // warps per lock-step group, 0 = none
-        if (grp >= nwarps || nwarps % grp != 0) {
+        if (grp == 0) {
+            // free-running warps
+        } else if (grp >= nwarps || nwarps % grp != 0) {
             __syncthreads();
-        } else if (grp > 0) {
+        } else {
             asm volatile("bar.sync %0, %1;" ::"r"(1 + warp / grp), "r"(grp * 32) : "memory");
         }
     }
