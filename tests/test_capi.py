@@ -86,6 +86,12 @@ def test_uncompiled_shape_binds_generic_kernel():
     rc, h = _create(2, 9, 4, 20, 1, 1)
     assert rc == 0 and lib.rmfht_plan_kernel(h) == 1
     lib.rmfht_plan_destroy(h)
+    # the specialised float32 kernels of the BASELINE shapes: pair kernel
+    # (r = 2, L = 2, M | 16), lane-group kernel (r = 2, L = 1, 4 | M)
+    for (r, m, L, M, kid) in [(2, 7, 2, 4, 6), (2, 7, 2, 3, 2), (2, 9, 1, 512, 7), (2, 9, 1, 6, 2)]:
+        rc, h = _create(r, m, L, M)
+        assert rc == 0 and lib.rmfht_plan_kernel(h) == kid, (r, m, L, M)
+        lib.rmfht_plan_destroy(h)
 
 
 def test_workspace_bytes_contract():
