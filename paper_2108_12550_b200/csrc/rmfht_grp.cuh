@@ -64,7 +64,12 @@ struct alignas(16) GWS {
     MapR<MM> comp[kItems];  // composite root map of each item (init, then the winning trial)
     float lm[2 * kItems];
     int dir[2 * kItems];
-    float lmp[2 * kItems][32];
+    // the transforms' transpose rows (fht_leaf, V >= 8); the LM lane partials
+    // of the root permutation extension are dead by then and share the space
+    union alignas(16) {
+        float wsp[32][32];
+        float lmp[2 * kItems][32];
+    };
 };
 
 template <int MM>
@@ -104,8 +109,10 @@ __device__ __forceinline__ float llr_abs(const float (&x)[V]) {
 // stage order, first bin of maximal |w|, metric and codeword bits.  bits:
 // bit k = hard decision of element k * 8 + u.
 template <int V>
-__device__ __forceinline__ u32 fht_leaf(const float (&x)[V], int u, float& pm, int& bin, int& sgn) {
+__device__ __forceinline__ u32 fht_leaf(const float (&x)[V], float (*wsp)[32], int lane, float& pm, int& bin,
+                                        int& sgn) {
     constexpr int n = V * kLpp;
+    const int g = lane >> 3, u = lane & 7;
     const float la = llr_abs<V>(x);
     float w[V];
 #pragma unroll
@@ -134,6 +141,38 @@ __device__ __forceinline__ u32 fht_leaf(const float (&x)[V], int u, float& pm, i
     };
 #pragma unroll
     for (int st = 0; st < clog2(V); st++) reg_stage(V >> (st + 1));
+    // TR (V >= 8): the vector is transposed through the warp's rows so that
+    // the lane-bit stages are register stages too — 16 wide shared accesses
+    // instead of 3 V shuffles (as rmfht2::FhtLayout::TR).  Afterwards slot
+    // j * G + q of lane u holds element (u * G + q) * 8 + j, G = V / 8.
+    constexpr bool TR = V >= 8;
+    constexpr int G = TR ? V / 8 : 1;
+    if constexpr (TR) {
+        // rows are lane-major, 16-byte chunks XOR-swizzled by the lane (and a
+        // per-group twist for V < 32): conflict-free STS.128 and transposed reads
+        const int tw = V == 16 ? 4 * (g & 1) : V == 8 ? 2 * g : 0;
+        auto at = [&](int row, int k) -> float& { return wsp[row][k ^ (((row & 7) ^ tw) << 2)]; };
+#pragma unroll
+        for (int k = 0; k < V; k += 4) *reinterpret_cast<float4*>(&at(lane, k)) = make_float4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const float* src = &at(g * 8 + j, u * G);
+            if constexpr (G == 4) {
+                const float4 v = *reinterpret_cast<const float4*>(src);
+                w[4 * j] = v.x; w[4 * j + 1] = v.y; w[4 * j + 2] = v.z; w[4 * j + 3] = v.w;
+            } else if constexpr (G == 2) {
+                const float2 v = *reinterpret_cast<const float2*>(src);
+                w[2 * j] = v.x; w[2 * j + 1] = v.y;
+            } else {
+                w[j] = *src;
+            }
+        }
+        __syncwarp();  // every row read before the next node stores
+        reg_stage(4 * G);
+        reg_stage(2 * G);
+        reg_stage(G);
+    } else {
     // lane stages (index bits 2, 1, 0)
 #pragma unroll
     for (int half = kLpp / 2; half >= 1; half >>= 1) {
@@ -152,6 +191,7 @@ __device__ __forceinline__ u32 fht_leaf(const float (&x)[V], int u, float& pm, i
             w[0] = __fmaf_rn(sg, w[0], o);
         }
     }
+    }
     float mx;
     {
         float t[V];
@@ -166,15 +206,21 @@ __device__ __forceinline__ u32 fht_leaf(const float (&x)[V], int u, float& pm, i
     const float M1 = group_max8(mx);
     pm = pm + 0.5f * (la - M1);  // :119
     // first bin of maximal |w| (stable argsort of -|w|, :116), with its sign
+    // (el: the lane's elements in ascending bin order; default layout: slot
+    // el is bin el * 8 + u, transposed: slot (el & 7) * G + (el >> 3) is bin
+    // u * V + el)
     int kk = V;
     float wv = 0.f;
 #pragma unroll
-    for (int k = V - 1; k >= 0; k--)
-        if (fabsf(w[k]) == M1) {
-            kk = k;
-            wv = w[k];
+    for (int el = V - 1; el >= 0; el--) {
+        const int s = TR ? (el & 7) * G + (el >> 3) : el;
+        if (fabsf(w[s]) == M1) {
+            kk = el;
+            wv = w[s];
         }
-    u32 key = kk < V ? (u32)((((kk << 3) | u) << 1) | (wv < 0.f ? 1 : 0)) : 0xffffffffu;
+    }
+    const int mybin = TR ? u * V + kk : ((kk << 3) | u);
+    u32 key = kk < V ? (u32)((mybin << 1) | (wv < 0.f ? 1 : 0)) : 0xffffffffu;
 #pragma unroll
     for (int off = 1; off < kLpp; off <<= 1) key = min(key, __shfl_xor_sync(kFull, key, off));
     bin = (int)(key >> 1);
@@ -252,10 +298,12 @@ __device__ __forceinline__ u32 spc_leaf8(float xv, int g, int u, float& pm) {
 // _decode_node (top_decoders.py:72-113) below the root: RM(RR, SS) on x[k] =
 // element k * 8 + u of this item's vector
 template <int RR, int SS>
-__device__ __forceinline__ u32 node(float (&x)[(1 << SS) / kLpp], int g, int u, float& pm, int& bin, int& sgn) {
+__device__ __forceinline__ u32 node(float (&x)[(1 << SS) / kLpp], float (*wsp)[32], int lane, float& pm, int& bin,
+                                    int& sgn) {
     constexpr int V = (1 << SS) / kLpp;
+    const int g = lane >> 3, u = lane & 7;
     if constexpr (RR == 1) {
-        return fht_leaf<V>(x, u, pm, bin, sgn);
+        return fht_leaf<V>(x, wsp, lane, pm, bin, sgn);
     } else if constexpr (RR == SS - 1) {
         static_assert(V == 1, "SPC leaf of r = 2 is RM(2, 3)");
         return spc_leaf8(x[0], g, u, pm);
@@ -265,11 +313,11 @@ __device__ __forceinline__ u32 node(float (&x)[(1 << SS) / kLpp], int g, int u, 
 #pragma unroll
         for (int k = 0; k < VC; k++) xl[k] = f_op(x[k], x[k + VC]);
         int cb, cs;
-        const u32 bl = node<RR - 1, SS - 1>(xl, g, u, pm, cb, cs);
+        const u32 bl = node<RR - 1, SS - 1>(xl, wsp, lane, pm, cb, cs);
         float xr[VC];
         static_assert(RR - 1 == 1, "r = 2: the left child is an FHT leaf");
         g_after_fht<VC>(cb, cs, u, x, x + VC, xr);
-        const u32 br = node<RR, SS - 1>(xr, g, u, pm, bin, sgn);
+        const u32 br = node<RR, SS - 1>(xr, wsp, lane, pm, bin, sgn);
         return (br << VC) | (bl ^ br);
     }
 }
@@ -382,7 +430,7 @@ __global__ void __launch_bounds__(32 * kGrpWarps, 1) grp_kernel(rmfht::Params<fl
                 for (int k = 0; k < VC; k++) xl[k] = f_op(lds_addr(ri.off(k)), lds_addr(ri.off(k + VC)));
             }
             int cb, cs;
-            const u32 bl = node<1, MM - 1>(xl, g, u, pm, cb, cs);
+            const u32 bl = node<1, MM - 1>(xl, ws.wsp, lane, pm, cb, cs);
             float xr[VC];
             {
                 rmfht2::RootIdx<MM, kLpp, V> ri;
@@ -406,7 +454,7 @@ __global__ void __launch_bounds__(32 * kGrpWarps, 1) grp_kernel(rmfht::Params<fl
                 g_after_fht<VC>(cb, cs, u, ga, gb, xr);
             }
             int db, ds;
-            const u32 br = node<2, MM - 1>(xr, g, u, pm, db, ds);
+            const u32 br = node<2, MM - 1>(xr, ws.wsp, lane, pm, db, ds);
             const u64 out = ((u64)br << VC) | (u64)(bl ^ br);
             if (u == 0) {
                 AttHdr h;
