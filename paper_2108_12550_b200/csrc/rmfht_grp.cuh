@@ -96,13 +96,30 @@ __device__ __forceinline__ float llr_abs(const float (&x)[V]) {
     for (int j = 0; j < J; j++) P[j] = fabsf(x[j]);
 #pragma unroll
     for (int k = J; k < V; k++) P[k & (J - 1)] += fabsf(x[k]);
+    // The xor tree over the lane bits 1, 2, 4 of every partial, transposed:
+    // at each level a lane keeps half of its partials and hands the other
+    // half to its partner, so the same sums (operands swapped at most: the
+    // addition commutes) take 6 shuffles instead of 12.  u: lane in the group.
+    const int u = threadIdx.x & 7;
+    if constexpr (J == 4) {
+        const bool b0 = u & 1, b1 = u & 2;
+        const float A = (b0 ? P[2] : P[0]) + __shfl_xor_sync(kFull, b0 ? P[0] : P[2], 1);
+        const float Bv = (b0 ? P[3] : P[1]) + __shfl_xor_sync(kFull, b0 ? P[1] : P[3], 1);
+        float C = (b1 ? Bv : A) + __shfl_xor_sync(kFull, b1 ? A : Bv, 2);  // partial 2 b0 + b1
+        C = C + __shfl_xor_sync(kFull, C, 4);
+        const float D = C + __shfl_xor_sync(kFull, C, 2);  // P0 + P1 (b0 = 0) or P2 + P3
+        return D + __shfl_xor_sync(kFull, D, 1);           // (P0 + P1) + (P2 + P3)
+    } else if constexpr (J == 2) {
+        const bool b0 = u & 1;
+        float A = (b0 ? P[1] : P[0]) + __shfl_xor_sync(kFull, b0 ? P[0] : P[1], 1);
+        A = A + __shfl_xor_sync(kFull, A, 2);
+        A = A + __shfl_xor_sync(kFull, A, 4);
+        return A + __shfl_xor_sync(kFull, A, 1);
+    } else {
 #pragma unroll
-    for (int off = 1; off < kLpp; off <<= 1)
-#pragma unroll
-        for (int j = 0; j < J; j++) P[j] = P[j] + __shfl_xor_sync(kFull, P[j], off);
-    if constexpr (J == 4) return (P[0] + P[1]) + (P[2] + P[3]);
-    else if constexpr (J == 2) return P[0] + P[1];
-    else return P[0];
+        for (int off = 1; off < kLpp; off <<= 1) P[0] = P[0] + __shfl_xor_sync(kFull, P[0], off);
+        return P[0];
+    }
 }
 
 // fhtl with one path (fht_decode.py:101-126): transform in the reference's
