@@ -741,10 +741,15 @@ __device__ __forceinline__ u64 fht_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
             const bool before = u < L && ((cq < cbest) || (cq == cbest && u < p));
             rank = __popc((__ballot_sync(kFull, before) >> (p * C::LPP)) & ((1u << L) - 1u));
         } else {
+            // fewer lanes per path than paths: L / LPP passes, lane u of every
+            // group comparing its path with path u + t LPP
+            static_assert(L % C::LPP == 0, "paths per pass");
 #pragma unroll
-            for (int q = 0; q < L; q++) {
+            for (int t = 0; t < L / C::LPP; t++) {
+                const int q = u + t * C::LPP;
                 const float cq = __shfl_sync(kFull, cbest, q * C::LPP);
-                rank += (cq < cbest) || (cq == cbest && q < p);
+                const bool before = (cq < cbest) || (cq == cbest && q < p);
+                rank += __popc((__ballot_sync(kFull, before) >> (p * C::LPP)) & ((1u << C::LPP) - 1u));
             }
         }
         // the one lane of each path holding a candidate (its maximum) records it
@@ -1041,15 +1046,38 @@ __device__ __forceinline__ u64 spc_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
     __syncwarp();
     // rank of each element in the stable ascending |alpha| order (:83); the
     // TAU+1 least reliable positions go to sord
+    // (full nodes of up to 16 elements: the path's magnitudes come in once as
+    // float4, and the index tie-break j < e is static except inside the
+    // element's own slot block — one compare per pair instead of three)
+    constexpr bool FASTRANK = LV::full && n <= 16 && n % 4 == 0;
+    float mg[FASTRANK ? n : 1];
+    if constexpr (FASTRANK) {
+#pragma unroll
+        for (int j = 0; j < n; j += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(&ws.smag[p * n + j]);
+            mg[j] = v.x; mg[j + 1] = v.y; mg[j + 2] = v.z; mg[j + 3] = v.w;
+        }
+    }
 #pragma unroll
     for (int k = 0; k < V; k++) {
         const int e = LV::full ? k * C::LPP + u : u;
         if (act) {
-            const float me = ws.smag[p * n + e];
             int rank = 0;
+            if constexpr (FASTRANK) {
+                const float me = fabsf(x[k]);
+#pragma unroll
+                for (int j = 0; j < n; j++) {
+                    const int jb = j / C::LPP, ju = j % C::LPP;
+                    if (jb < k) rank += mg[j] <= me;
+                    else if (jb > k) rank += mg[j] < me;
+                    else rank += (mg[j] < me) || (mg[j] == me && ju < u);
+                }
+            } else {
+            const float me = ws.smag[p * n + e];
             for (int j = 0; j < n; j++) {
                 const float mj = ws.smag[p * n + j];
                 rank += (mj < me) || (mj == me && j < e);
+            }
             }
             if (rank <= TAU) ws.sord[p * 16 + rank] = (uint16_t)e;
             // sign bit and the rank (capped at TAU + 1: only ranks 0..TAU are
@@ -1092,10 +1120,23 @@ __device__ __forceinline__ u64 spc_node(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32
         }
         // stable rank among the 2L candidates (:104), by shuffles
         int rank = 0;
+        if constexpr (2 * L == 16) {
+            // the upper half warp ranks a copy of each candidate against the
+            // candidates 8 .. 15 while the lower half takes 0 .. 7
+            const int ci = lane & 15, h8 = (lane >> 4) * 8;
+            const float mine = __shfl_sync(kFull, cand, ci);
 #pragma unroll
-        for (int c = 0; c < 2 * L; c++) {
-            const float pc = __shfl_sync(kFull, cand, c);
-            rank += (pc < cand) || (pc == cand && c < lane);
+            for (int c = 0; c < 8; c++) {
+                const float pc = __shfl_sync(kFull, cand, h8 + c);
+                rank += (pc < mine) || (pc == mine && h8 + c < ci);
+            }
+            rank += __shfl_xor_sync(kFull, rank, 16);
+        } else {
+#pragma unroll
+            for (int c = 0; c < 2 * L; c++) {
+                const float pc = __shfl_sync(kFull, cand, c);
+                rank += (pc < cand) || (pc == cand && c < lane);
+            }
         }
         // no flip survives and the keeps are already in slot order: the state
         // is unchanged, and since the later positions are at least as
