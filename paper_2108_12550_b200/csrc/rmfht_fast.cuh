@@ -144,7 +144,7 @@ struct alignas(16) WS2 {
     alignas(16) uint16_t recs[RB][(RECW + 7) & ~7];  // cp.async prefetch; the item's maps
     MapR<MM> comp[L];  // composite map of each root path (root perm-ext winners)
     float pm[L], llrabs[L];
-    float lm[2 * L];
+    alignas(16) float lm[2 * L];
     static constexpr int CA = kCap > L * L ? kCap : L * L;  // candidate list (and the exact fallback)
     static constexpr int CB = L * L > 2 * L ? L * L : 2 * L;  // per path / per split / fallback pool
     float cw[CA], cpm[CB];  // candidate values (|w| = fabsf(cw)), pool pms
@@ -1273,7 +1273,19 @@ template <int R, int MM, int L>
 __device__ __forceinline__ void select_trials2(Ctx2<R, MM, L>& cx) {
     auto& ws = cx.ws;
     const int lane = cx.lane;
-    if (lane < 2 * L) {
+    if constexpr (2 * L == 16) {
+        // both half warps rank a copy of each trial, against 8 trials each
+        // (two LDS.128 per lane instead of 16 scalar loads)
+        const int ci = lane & 15, h8 = (lane >> 4) * 8;
+        const float v = ws.lm[ci];
+        const float4 a = *reinterpret_cast<const float4*>(&ws.lm[h8]), b = *reinterpret_cast<const float4*>(&ws.lm[h8 + 4]);
+        const float o[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        int rank = 0;
+#pragma unroll
+        for (int s = 0; s < 8; s++) rank += (o[s] > v) || (o[s] == v && h8 + s < ci);
+        rank += __shfl_xor_sync(kFull, rank, 16);
+        if (lane < 16 && rank < L) ws.ord[rank] = (int8_t)lane;
+    } else if (lane < 2 * L) {
         const float v = ws.lm[lane];
         int rank = 0;
 #pragma unroll
