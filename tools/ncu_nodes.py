@@ -98,24 +98,76 @@ def main():
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     h = rows[1]
-    iA, iE = h.index("Address"), h.index("Instructions Executed")
+    iA, iE, iS = h.index("Address"), h.index("Instructions Executed"), h.index("Source")
     iW = h.index("L1 Wavefronts Shared") if "L1 Wavefronts Shared" in h else None
-    execs = [(int(r[iA], 16), int(float(r[iE] or 0)), int(float(r[iW] or 0)) if iW is not None else 0)
+    execs = [(int(r[iA], 16), int(float(r[iE] or 0)), int(float(r[iW] or 0)) if iW is not None else 0, r[iS])
              for r in rows[2:] if len(r) > iE and r[iA].startswith("0x")]
     base = execs[0][0]
     ch = chains(obj, ksub)
     roles = call_lines()
     cnt, wav = collections.Counter(), collections.Counter()
-    for a, n, w in execs:
+    cls = collections.defaultdict(collections.Counter)
+    for a, n, w, sass in execs:
         c = ch.get(a - base)
         key = label(c, roles, mm) if c is not None else "unmapped"
         cnt[key] += n
         wav[key] += w
+        cls[key][opclass(sass)] += n
     tot = sum(cnt.values())
     print(f"warp instructions per item: {tot / items:.0f}; shared wavefronts per item: {sum(wav.values()) / items:.0f}")
-    print(f"{'node':40s} {'instr/item':>10s} {'share':>7s} {'wavefronts/item':>16s}")
+    print("classes: fp = FADD/FADD2/FFMA/FFMA2/FMUL/FMUL2/FMNMX/FMNMX3 (the ledger's additions and comparisons; a "
+          "packed instruction counts once), fpsel = FSETP/FSEL (candidate tests and selects), mio = LDS/STS/SHFL/"
+          "LDGSTS/LDG/STG/ATOM, ctl = everything else (integer, logic, moves, predicates, branches, votes)")
+    print("ledger: the reference ledger's operations of the node (n log2 n per FHT, n/2 per f and g, per path; "
+          "LM of the 2L root trials) / 32 lanes = the instructions an ideal scalar-per-lane kernel would issue")
+    print(f"{'node':34s} {'instr/item':>10s} {'share':>6s} {'fp':>6s} {'fpsel':>6s} {'mio':>6s} {'ctl':>6s} {'wavefr':>7s} {'ledger':>7s}")
     for k in sorted(cnt, key=lambda k: (-cnt[k])):
-        print(f"{k:40s} {cnt[k] / items:10.1f} {100 * cnt[k] / tot:6.1f}% {wav[k] / items:16.1f}")
+        c = cls[k]
+        led = ledger_floor(k, mm)
+        print(f"{k:34s} {cnt[k] / items:10.1f} {100 * cnt[k] / tot:5.1f}% {c['fp'] / items:6.0f} {c['fpsel'] / items:6.0f} "
+              f"{c['mio'] / items:6.0f} {c['ctl'] / items:6.0f} {wav[k] / items:7.1f} {led if led is not None else '':>7}")
+    c = collections.Counter()
+    for k in cls:
+        c.update(cls[k])
+    print(f"{'total':34s} {tot / items:10.1f} {'':6s} {c['fp'] / items:6.0f} {c['fpsel'] / items:6.0f} {c['mio'] / items:6.0f} "
+          f"{c['ctl'] / items:6.0f} {sum(wav.values()) / items:7.1f}")
+
+
+FP = ("FADD", "FFMA", "FMUL", "FMNMX")
+MIO = ("LDS", "STS", "SHFL", "LDGSTS", "LDG", "STG", "ATOM", "RED", "LDL", "STL", "LD.", "ST.")
+
+
+def opclass(sass):
+    t = sass.split()
+    if not t:
+        return "ctl"
+    op = t[1] if t[0].startswith("@") and len(t) > 1 else t[0]
+    if op.startswith(FP):
+        return "fp"
+    if op.startswith(("FSETP", "FSEL", "FSET")):
+        return "fpsel"
+    if op.startswith(MIO):
+        return "mio"
+    return "ctl"
+
+
+def ledger_floor(name, mm, L=4):
+    """the reference ledger's operation count of a tree node (accounting.py:136-152: n log2 n per
+    FHT, n/2 per f and per g, per path) in warp instructions (/ 32)"""
+    m = re.search(r"n=(\d+)", name)
+    if name == "root perm-ext":
+        n = 1 << mm
+        return round(2 * L * n / 32)  # 2L trials x (n/2 minima + n/2 additions)
+    if not m:
+        return None
+    n = int(m.group(1))
+    if name.endswith("FHT"):
+        return round(L * n * (n.bit_length() - 1) / 32)
+    if name.endswith("glue"):
+        return round(L * n / 32)  # f and g: n/2 each
+    if name.endswith("SPC"):
+        return round(L * 2 * n / 32)
+    return None
 
 
 if __name__ == "__main__":
