@@ -84,3 +84,25 @@ def test_att_cw_without_att_pm():
     assert rc == 0
     torch.cuda.synchronize()
     assert np.array_equal(out["att_cw"].cpu().numpy().view(np.uint32), full["att_cw_packed"])
+
+
+def test_free_running_warps_decode_the_same():
+    """RMFHT_LOCKSTEP_GROUP=0 (A/B hook: no round barrier in the throughput
+    kernel) changes the schedule, not the results."""
+    import os
+    from paper_2108_12550_b200.channel_model import synthetic_frames
+    from paper_2108_12550_b200.decoder import Plan
+    from paper_2108_12550_b200.rm_core import build_code
+    spec = build_code(2, 9)
+    _, llr = synthetic_frames(spec, 2.0, 700, seed=21)
+    plan = Plan(2, 9, 4, 20, True, "f32")
+    os.environ["RMFHT_LOCKSTEP_GROUP"] = "0"
+    try:
+        free = Plan(2, 9, 4, 20, True, "f32")
+    finally:
+        del os.environ["RMFHT_LOCKSTEP_GROUP"]
+    _, rec = plan.sample(700, seed=8)
+    a = plan.decode(llr, records=rec, diag=True)
+    b = free.decode(llr, records=rec, diag=True)
+    for k in ("cw", "pm", "attempt", "path", "att_pm", "att_cw"):
+        assert np.array_equal(a[k], b[k]), k

@@ -53,5 +53,11 @@ def test_gpu_harness_zero_noise_and_rank_invariance():
     a = harness.run_job(harness.SimJob(r=2, m=7, decoder=DecoderConfig("p-FHT-FSCL", L=2, M=4), ebn0_points=(2.0,),
                                        max_frames=20000, min_frame_errors=10 ** 9, batch=4000))[0]
     b = harness.run_job(harness.SimJob(r=2, m=7, decoder=DecoderConfig("p-FHT-FSCL", L=2, M=4), ebn0_points=(2.0,),
-                                       max_frames=20000, min_frame_errors=10 ** 9, batch=4000))[0]
+                                       max_frames=20000, min_frame_errors=10 ** 9, batch=2500))[0]
     assert (a.frames, a.frame_errors, a.ml_lb_fer) == (b.frames, b.frame_errors, b.ml_lb_fer)
+    # (frames and permutation tables are keyed by the frame index, not by the batch that draws them)
+    c = harness.run_job(harness.SimJob(r=2, m=9, decoder=DecoderConfig("p-FHT-FSCL", L=1, M=512), ebn0_points=(2.0,),
+                                       max_frames=3000, min_frame_errors=10 ** 9, batch=1000))[0]
+    d = harness.run_job(harness.SimJob(r=2, m=9, decoder=DecoderConfig("p-FHT-FSCL", L=1, M=512), ebn0_points=(2.0,),
+                                       max_frames=3000, min_frame_errors=10 ** 9, batch=768))[0]
+    assert (c.frames, c.frame_errors, c.ml_lb_fer) == (d.frames, d.frame_errors, d.ml_lb_fer)
