@@ -79,7 +79,7 @@ __device__ __forceinline__ void draw_store(uint64_t key, Put&& put, Put16&& put1
     for (int j = 0; j < MN; j++) {
         const unsigned coef = ub[j] >> 16;
         put16(MG + 1 + (__ffs(pv[j]) - 1), coef);
-        if (b & pv[j]) c ^= coef;  // A^-1 b = sum over the set bits k of b of column k
+        rmfht_maps::xor_if(c, b, pv[j], coef);  // A^-1 b = sum over the set bits k of b of column k
     }
     put16(2 * MG + 1, c);
 }
@@ -173,14 +173,15 @@ __global__ void __launch_bounds__(256) sample_kernel(SampleArgs a, uint32_t* rec
 // = (t / S, t % S) of the table (item-major, the record order in memory), so
 // the 32 lanes of a warp draw 32 consecutive records and every thread has
 // exactly one draw — no idle warps, no CTA barrier.  A warp stages its 32
-// records in its own shared-memory rows (record stride W + 1 words: odd,
-// conflict-free) and writes them out as 32 x W contiguous words (coalesced
-// 32-bit stores).  Same draws as sample_kernel (draw_store: bit-identical
+// records in its own shared-memory row in memory order (record stride W
+// words: the per-lane stores take a two-way bank conflict for even W, the
+// write-out needs no index arithmetic) and writes them out as 32 x W
+// contiguous words (coalesced 32-bit stores).  Same draws as sample_kernel (draw_store: bit-identical
 // tables).
 template <int MG>
 __global__ void __launch_bounds__(256) sample_kernel_flat(SampleArgs a, uint32_t* rec) {
     constexpr int W = MG + 1;
-    __shared__ uint32_t stage[8][32 * (W + 1)];
+    __shared__ uint32_t stage[8][32 * W];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const long long tasks = a.B * (long long)a.M * a.S;
     uint32_t* st = stage[warp];
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(256) sample_kernel_flat(SampleArgs a, uint32_t
                 at = (int)(item % a.M);
             }
             f += a.frame0;
-            uint32_t* dst = st + lane * (W + 1);
+            uint32_t* dst = st + lane * W;
             auto put = [&](int w, unsigned v) { dst[w] = v; };
             auto put16 = [&](int hw, unsigned v) { reinterpret_cast<uint16_t*>(dst)[hw] = (uint16_t)v; };
             const int mn = a.sizes[s];
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(256) sample_kernel_flat(SampleArgs a, uint32_t
 #pragma unroll
         for (int j = 0; j < W; j++) {
             const int o = j * 32 + lane;  // word o of the warp's n * W words
-            if (o < n * W) out[o] = st[(o / W) * (W + 1) + o % W];
+            if (o < n * W) out[o] = st[o];
         }
         __syncwarp();
     }

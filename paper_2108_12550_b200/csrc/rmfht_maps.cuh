@@ -104,6 +104,19 @@ struct Word16 {
     }
 };
 
+// t ^= u when (v & m) != 0
+RMFHT_HD void xor_if(unsigned& t, unsigned v, unsigned m, unsigned u) {
+#ifdef __CUDA_ARCH__
+    // a predicated XOR (two instructions; the compiler's own choice was test,
+    // select, XOR — the sampler kernel is issue-bound on exactly these)
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 q;\n\tand.b32 q, %1, %2;\n\tsetp.ne.u32 p, q, 0;\n\t@p xor.b32 %0, %0, %3;\n\t}"
+        : "+r"(t)
+        : "r"(v), "r"(m), "r"(u));
+#else
+    if (v & m) t ^= u;
+#endif
+}
+
 // Uniform (A, b) in GL(MN,2) x F_2^MN — the distribution of the reference's
 // rejection sampler (automorphism.py:127-161) — drawn column by column, each
 // column uniform over the vectors outside the span of the previous ones, so
@@ -138,15 +151,13 @@ RMFHT_HD void draw_map_basis(uint64_t key, unsigned (&cols)[MN], unsigned (&ub)[
         } while (r == 0u);
         unsigned t = 0u;
 #pragma unroll
-        for (int j = 0; j < i; j++)
-            if (v & pv[j]) t ^= ub[j];
+        for (int j = 0; j < i; j++) xor_if(t, v, pv[j], ub[j]);
         cols[i] = r ^ (t & 0xffffu);
         ub[i] = (r | (1u << (16 + i))) ^ (t & 0xffff0000u);
         pv[i] = r & (0u - r);
         pivm |= pv[i];
 #pragma unroll
-        for (int j = 0; j < i; j++)
-            if (ub[j] & pv[i]) ub[j] ^= ub[i];
+        for (int j = 0; j < i; j++) xor_if(ub[j], ub[j], pv[i], ub[i]);
     }
     b = rs.next() & mask;
 }
