@@ -59,7 +59,7 @@ struct SampleArgs {
 template <int MN, int MG, typename Put, typename Put16>
 __device__ __forceinline__ void draw_store(uint64_t key, Put&& put, Put16&& put16) {
     unsigned cols[MN], ub[MN], pv[MN], b;
-    rmfht_maps::draw_map_basis<MN>(key, cols, ub, pv, b);
+    rmfht_maps::draw_map_basis<MN, rmfht_maps::Word16p>(key, cols, ub, pv, b);
     // record halves: cols of A (MG), b, cols of A^-1 (MG), A^-1 b; whole
     // words up to half MG, half words after (never both on one location)
     unsigned h[MG + 2];

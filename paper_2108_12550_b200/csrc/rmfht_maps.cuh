@@ -104,6 +104,34 @@ struct Word16 {
     }
 };
 
+// The same word stream with its first four splitmix64 outputs drawn up front
+// (device sampler): the lanes of a warp fall out of step after a redraw, and
+// Word16's refill — a whole splitmix64 behind a divergent branch at every call
+// site — then ran at nearly every call of every warp; here the refill picks
+// one of the four prepared words (a fifth, after more than six redraws in one
+// map, is drawn on the spot).
+struct Word16p {
+    uint64_t st, w, w1, w2, w3;
+    int left, fills;
+    RMFHT_HD explicit Word16p(uint64_t key) : st(key), left(4), fills(1) {
+        w = splitmix64(st);
+        w1 = splitmix64(st);
+        w2 = splitmix64(st);
+        w3 = splitmix64(st);
+    }
+    RMFHT_HD unsigned next() {
+        if (left == 0) {
+            w = fills == 1 ? w1 : fills == 2 ? w2 : fills == 3 ? w3 : splitmix64(st);
+            fills++;
+            left = 4;
+        }
+        const unsigned v = (unsigned)w & 0xffffu;
+        w >>= 16;
+        left--;
+        return v;
+    }
+};
+
 // t ^= u when (v & m) != 0
 RMFHT_HD void xor_if(unsigned& t, unsigned v, unsigned m, unsigned u) {
 #ifdef __CUDA_ARCH__
@@ -136,10 +164,10 @@ RMFHT_HD void xor_if(unsigned& t, unsigned v, unsigned m, unsigned u) {
 // e_i ^ sum_{j: s_j} coef_j, and eliminating p_i from the earlier u_j XORs
 // both halves.  After MN columns the u_j are the unit vectors e_{p_j}, so
 // A^-1 e_{p_j} = coef_j: the columns of A^-1 without a Gauss-Jordan pass.
-template <int MN>
+template <int MN, typename Words = Word16>
 RMFHT_HD void draw_map_basis(uint64_t key, unsigned (&cols)[MN], unsigned (&ub)[MN], unsigned (&pv)[MN], unsigned& b) {
     constexpr unsigned mask = (1u << MN) - 1u;
-    Word16 rs(key);
+    Words rs(key);
     // ub: basis word (u | coef << 16), pv: its pivot bit
     unsigned pivm = 0u;
 #pragma unroll
