@@ -52,7 +52,7 @@ int fail(int code, const std::string& msg);
 // tests exercise.  Split into chunks that compile in
 // parallel (rmfht_bind.cu is built once per dtype x chunk).
 #define RMFHT_CHUNK0(X) X(2, 9, 4) X(2, 5, 1) X(1, 2, 4) X(3, 4, 4)
-#define RMFHT_CHUNK1(X) X(3, 7, 8) X(2, 4, 2) X(1, 5, 4)
+#define RMFHT_CHUNK1(X) X(3, 7, 8) X(2, 4, 2) X(1, 5, 4) X(2, 8, 1)
 #define RMFHT_CHUNK2(X) X(2, 9, 1) X(2, 7, 2) X(2, 6, 4) X(2, 6, 1)
 #define RMFHT_CHUNK3(X) X(2, 8, 8) X(3, 8, 4) X(2, 9, 2) X(3, 6, 2) X(2, 5, 4)
 #define RMFHT_NCHUNKS 4

@@ -70,3 +70,25 @@ def test_grp_kernel_only_when_attempts_divide():
     assert Plan(2, 9, 1, 6, True, "f32").kernel == 2
     assert Plan(2, 9, 1, 512, True, "f64").kernel == 1
     assert Plan(2, 9, 1, 1, False, "f32").kernel == 2  # FHT-FSC: no permutations
+
+
+@pytest.mark.parametrize("M,B", [(4, 2000), (16, 600)])
+def test_grp_kernel_rm28(M, B, oracle_mod):
+    """The m = 8 instantiation (N = 256): against the throughput kernel and the oracle."""
+    from paper_2108_12550_b200.channel_model import synthetic_frames
+    from paper_2108_12550_b200.decoder import Plan
+    from paper_2108_12550_b200.rm_core import build_code
+    spec = build_code(2, 8)
+    _, llr = synthetic_frames(spec, 2.0, B, seed=40 + M)
+    plan = Plan(2, 8, 1, M, True, "f32")
+    assert plan.kernel == 7
+    ref = _throughput_plan(2, 8, 1, M, True, "f32")
+    assert ref.kernel == 2
+    raw, rec = plan.sample(B, seed=M)
+    a = plan.decode(llr, records=rec, diag=True)
+    b = ref.decode(llr, records=rec, diag=True)
+    for k in ("cw", "pm", "attempt", "path", "att_pm", "att_cw"):
+        assert np.array_equal(a[k], b[k]), k
+    c = oracle_mod.decode(2, 8, 1, M, llr[:300], raw[:300], dtype=np.float32, nthreads=16, order="v2")
+    for k in ("cw", "pm", "attempt", "att_pm"):
+        assert np.array_equal(a[k][:300], c[k]), k
