@@ -92,3 +92,23 @@ def test_grp_kernel_rm28(M, B, oracle_mod):
     c = oracle_mod.decode(2, 8, 1, M, llr[:300], raw[:300], dtype=np.float32, nthreads=16, order="v2")
     for k in ("cw", "pm", "attempt", "att_pm"):
         assert np.array_equal(a[k][:300], c[k]), k
+
+
+@pytest.mark.parametrize("B", [1, 2, 3, 33])
+def test_grp_kernel_small_and_ragged_batches(B):
+    """Batches smaller than a CTA round and not a multiple of anything: every
+    frame still gets its own answer (against the throughput kernel)."""
+    from paper_2108_12550_b200.channel_model import synthetic_frames
+    from paper_2108_12550_b200.decoder import Plan
+    from paper_2108_12550_b200.rm_core import build_code
+    spec = build_code(2, 9)
+    _, llr = synthetic_frames(spec, 1.0, B, seed=B)
+    for M in (4, 512):
+        plan = Plan(2, 9, 1, M, True, "f32")
+        ref = _throughput_plan(2, 9, 1, M, True, "f32")
+        assert (plan.kernel, ref.kernel) == (7, 2)
+        _, rec = plan.sample(B, seed=B + M)
+        a = plan.decode(llr, records=rec, diag=True)
+        b = ref.decode(llr, records=rec, diag=True)
+        for k in ("cw", "pm", "attempt", "path", "att_pm", "att_cw"):
+            assert np.array_equal(a[k], b[k]), (k, M)
