@@ -1285,6 +1285,15 @@ __device__ __forceinline__ void select_trials2(Ctx2<R, MM, L>& cx) {
         for (int s = 0; s < 8; s++) rank += (o[s] > v) || (o[s] == v && h8 + s < ci);
         rank += __shfl_xor_sync(kFull, rank, 16);
         if (lane < 16 && rank < L) ws.ord[rank] = (int8_t)lane;
+    } else if constexpr (2 * L == 8) {
+        // the four quarter warps rank a copy of each trial against two trials each
+        const int ci = lane & 7, q2 = (lane >> 3) * 2;
+        const float v = ws.lm[ci];
+        const float2 o = *reinterpret_cast<const float2*>(&ws.lm[q2]);
+        int rank = ((o.x > v) || (o.x == v && q2 < ci)) + ((o.y > v) || (o.y == v && q2 + 1 < ci));
+        rank += __shfl_xor_sync(kFull, rank, 8);
+        rank += __shfl_xor_sync(kFull, rank, 16);
+        if (lane < 8 && rank < L) ws.ord[rank] = (int8_t)lane;
     } else if (lane < 2 * L) {
         const float v = ws.lm[lane];
         int rank = 0;
