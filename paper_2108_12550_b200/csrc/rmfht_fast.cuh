@@ -978,10 +978,20 @@ __device__ __forceinline__ u64 spc_node_v1(Ctx2<R, MM, L>& cx, float xv, int8_t*
             }
         }
         int r2 = 0;
+        if constexpr (2 * L == 8) {
+            // the four quarter warps rank a copy of each candidate against two candidates each
+            const int ci = lane & 7, q2 = (lane >> 3) * 2;
+            const float mine = __shfl_sync(kFull, cand, ci);
+            const float c0 = __shfl_sync(kFull, cand, q2), c1 = __shfl_sync(kFull, cand, q2 + 1);
+            r2 = ((c0 < mine) || (c0 == mine && q2 < ci)) + ((c1 < mine) || (c1 == mine && q2 + 1 < ci));
+            r2 += __shfl_xor_sync(kFull, r2, 8);
+            r2 += __shfl_xor_sync(kFull, r2, 16);
+        } else {
 #pragma unroll
-        for (int c = 0; c < 2 * L; c++) {
-            const float cc = __shfl_sync(kFull, cand, c);
-            r2 += (cc < cand) || (cc == cand && c < lane);
+            for (int c = 0; c < 2 * L; c++) {
+                const float cc = __shfl_sync(kFull, cand, c);
+                r2 += (cc < cand) || (cc == cand && c < lane);
+            }
         }
         // no flip survives and the keeps are already in slot order: the state
         // is unchanged, and since the later positions are at least as
