@@ -199,6 +199,7 @@ struct Ctx2 {
     int lane, p, u;
     u32 alpha_saddr;           // shared-window address of alpha (2 KB aligned)
     int ngen;                  // RMFHT_STATS only: FHT nodes of this item off the common case
+    u32 tmem;                  // this warp's tensor-memory block (tmem_park), lane quadrant and first column
 };
 
 // ------------------------------------------------------------ helpers ----
@@ -1573,6 +1574,49 @@ __device__ __forceinline__ u64 node2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / 
     }
 }
 
+// ------------------------------------------------- tensor-memory parking ----
+// The root's g (:104) needs the same 2 VC channel LLRs per lane that its f
+// (:100) gathered a whole left subtree earlier; there are no registers to
+// keep them and no shared memory left, so the kernel gathered them twice —
+// VC * 2 bank-conflicted LDS per lane, a fifth of the kernel's shared-memory
+// wavefronts.  Blackwell's tensor memory (256 KB per SM, unused by a kernel
+// without MMAs) holds them instead: f's gathers are stored with tcgen05.st
+// (32 lanes x 32-bit columns, a warp's own lane quadrant, its own column
+// block) and g reads them back with tcgen05.ld; when the left child re-ordered
+// the paths, the values come from the source path's lanes by shuffles.
+#ifndef RMFHT_NO_TMEM
+#define RMFHT_TMEM_PARK 1
+#else
+#define RMFHT_TMEM_PARK 0
+#endif
+template <int R, int MM, int L>
+__host__ __device__ constexpr bool tmem_park() {
+    // the root's left child is an FHT leaf (R == 2), 8 lanes per path, 32 slots per half
+    return RMFHT_TMEM_PARK && R == 2 && MM >= 3 && (32 / L) == 8 && ((1 << (MM - 1)) / (32 / L)) == 32;
+}
+__device__ __forceinline__ void tmem_st8(u32 taddr, const float* v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+                 "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+                 "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+                 "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(u32 taddr, u32* r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr)
+                 : "memory");
+}
+// the loaded registers may only be read after the wait: they pass through it
+__device__ __forceinline__ void tmem_wait_ld16(u32* a, u32* b) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
+                   "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]), "+r"(b[7])
+                 :
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 // ------------------------------------------------------------ root node ----
 // Internal root (1 < r < m-1): the root vectors are never held; f (:100) and
 // g (:104) read them straight from the frame LLRs through each path's
@@ -1597,8 +1641,28 @@ __device__ __forceinline__ u64 root_node(Ctx2<R, MM, L>& cx, int8_t* lin, F&& al
 #endif
         RootIdx<MM, C::LPP, LV::V> ri;
         ri.build(ws.comp[p], u, cx.alpha_saddr);
+        if constexpr (tmem_park<R, MM, L>()) {
+            // gather, park both halves in tensor memory (column k: the lower
+            // half's slot k, column VC + k the upper half's), then f
 #pragma unroll
-        for (int k = 0; k < VC; k++) xl[k] = f_op(lds_addr(ri.off(k)), lds_addr(ri.off(k + VC)));
+            for (int k0 = 0; k0 < VC; k0 += 8) {
+                float a[8], b[8];
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    a[i] = lds_addr(ri.off(k0 + i));
+                    b[i] = lds_addr(ri.off(k0 + i + VC));
+                }
+                tmem_st8(cx.tmem + k0, a);
+                tmem_st8(cx.tmem + VC + k0, b);
+#pragma unroll
+                for (int i = 0; i < 8; i++) xl[k0 + i] = f_op(a[i], b[i]);
+            }
+            tmem_wait_st();
+            alpha_dead();  // the frame LLRs are not read again
+        } else {
+#pragma unroll
+            for (int k = 0; k < VC; k++) xl[k] = f_op(lds_addr(ri.off(k)), lds_addr(ri.off(k + VC)));
+        }
 #ifdef RMFHT_STATS
         {
             float z = 0.f;
@@ -1614,7 +1678,51 @@ __device__ __forceinline__ u64 root_node(Ctx2<R, MM, L>& cx, int8_t* lin, F&& al
     }
     const u64 bl = node2<R, MM, L, R - 1, MM - 1, true>(cx, xl, l1);
     float xr[VC];
-    {
+    if constexpr (tmem_park<R, MM, L>()) {
+        // g (:104) from the parked values of the source path (:102); the
+        // factors follow g_fht_child's Gray-code walk, whose steps 4 c .. 4 c + 3
+        // stay inside the 8-slot chunk c ^ (c >> 1)
+        const int src1 = l1[p];
+        const bool moved = __any_sync(kFull, src1 != p);
+        const int from = src1 * C::LPP + u;
+        constexpr int n = 1 << (MM - 1);
+        const int bin = ws.sel_bin[p];
+        const int sgn = ws.sel_w[p] < 0.f;
+        const u32 B = (u32)(~bin) & (u32)(n - 1);
+        const u32 Bh = B >> C::LB;
+        const int c0 = sgn ^ (__popc(B) & 1) ^ (__popc(B & (u32)u & (u32)(C::LPP - 1)) & 1);
+        const float base = c0 ? -1.f : 1.f;
+        const float col0 = (Bh & 1u) ? -1.f : 1.f;
+        u64 s2 = pk(base, base * col0);
+#pragma unroll
+        for (int c = 0; c < VC / 8; c++) {
+            const int k0 = 8 * (c ^ (c >> 1));
+            u32 ra[8], rb[8];
+            tmem_ld8(cx.tmem + k0, ra);
+            tmem_ld8(cx.tmem + VC + k0, rb);
+            tmem_wait_ld16(ra, rb);
+            if (moved) {
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    ra[i] = __shfl_sync(kFull, ra[i], from);
+                    rb[i] = __shfl_sync(kFull, rb[i], from);
+                }
+            }
+#pragma unroll
+            for (int i = 4 * c; i < 4 * c + 4; i++) {
+                if (i > 0) {
+                    const int j = __ffs(i);
+                    const float cj = ((Bh >> j) & 1u) ? -1.f : 1.f;
+                    s2 = mul2(s2, pk(cj, cj));
+                }
+                const int k = 2 * (i ^ (i >> 1)), q = k - k0;
+                const u64 r = fma2(s2, pk(__uint_as_float(ra[q]), __uint_as_float(ra[q + 1])),
+                                   pk(__uint_as_float(rb[q]), __uint_as_float(rb[q + 1])));
+                xr[k] = plo(r);
+                xr[k + 1] = phi(r);
+            }
+        }
+    } else {
         RootIdx<MM, C::LPP, LV::V> ri;
         ri.build(ws.comp[l1[p]], u, cx.alpha_saddr);
         if constexpr (R - 1 == 1 && VC >= 2) {
@@ -1711,6 +1819,25 @@ __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Par
     Ctx2<R, MM, L> cx{ws, alpha_w, nullptr, PM ? 1 : 0, {}, lane, lane / C::LPP, lane % C::LPP, asa};
     static_assert(sizeof(MapR<MM>) == 2 * (2 * MM + 2), "record layout");
     constexpr bool ROOT_INTERNAL = !(R == 1 || R == MM - 1);
+    // tensor memory for the root's parked gathers (tmem_park): the whole 512
+    // columns (one CTA per SM); warp w owns lanes 32 (w % 4) .. + 31 (the
+    // quadrant a warp may access) and columns 64 (w / 4) .. + 63
+    constexpr bool TPARK = PM && ROOT_INTERNAL && tmem_park<R, MM, L>();
+    __shared__ u32 tmem_slot;
+    cx.tmem = 0;
+    if constexpr (TPARK) {
+        static_assert((nwarps + 3) / 4 * 64 <= 512, "tensor-memory columns");
+        if (warp == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                             (u32)__cvta_generic_to_shared(&tmem_slot))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        cx.tmem = tmem_slot + ((u32)(32 * (warp & 3)) << 16) + (u32)(64 * (warp >> 2));
+    }
     // items < 2^31 per launch (launch_fast splits larger batches)
     const int items = (int)prm.B * prm.M;
     const int stride = (int)gridDim.x * nwarps;
@@ -1827,6 +1954,11 @@ __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Par
         } else {
             asm volatile("bar.sync %0, %1;" ::"r"(1 + warp / grp), "r"(grp * 32) : "memory");
         }
+    }
+    if constexpr (TPARK) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_slot) : "memory");
     }
 }
 
