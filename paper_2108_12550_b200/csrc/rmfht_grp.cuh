@@ -286,6 +286,42 @@ __device__ __forceinline__ void g_after_fht(int bin, int sgn, int u, const float
     }
 }
 
+// The root's g from its gathers parked in tensor memory (rmfht2::tmem_park):
+// column k holds the lower half's slot k, column V + k the upper half's; the
+// Gray-code steps 4 c .. 4 c + 3 stay inside the 8-slot chunk c ^ (c >> 1).
+template <int V>
+__device__ __forceinline__ void g_after_fht_tmem(int bin, int sgn, int u, u32 taddr, float* out) {
+    static_assert(V >= 8 && V % 8 == 0, "8-column chunks");
+    constexpr int n = V * kLpp;
+    const u32 B = (u32)(~bin) & (u32)(n - 1);
+    const u32 Bh = B >> 3;
+    const int c0 = sgn ^ (__popc(B) & 1) ^ (__popc(B & (u32)u & 7u) & 1);
+    const float base = c0 ? -1.f : 1.f;
+    const float col0 = (Bh & 1u) ? -1.f : 1.f;
+    u64 s2 = pk(base, base * col0);
+#pragma unroll
+    for (int c = 0; c < V / 8; c++) {
+        const int k0 = 8 * (c ^ (c >> 1));
+        u32 ra[8], rb[8];
+        rmfht2::tmem_ld8(taddr + k0, ra);
+        rmfht2::tmem_ld8(taddr + V + k0, rb);
+        rmfht2::tmem_wait_ld16(ra, rb);
+#pragma unroll
+        for (int i = 4 * c; i < 4 * c + 4; i++) {
+            if (i > 0) {
+                const int j = __ffs(i);
+                const float cj = ((Bh >> j) & 1u) ? -1.f : 1.f;
+                s2 = mul2(s2, pk(cj, cj));
+            }
+            const int k = 2 * (i ^ (i >> 1)), q = k - k0;
+            const u64 r = fma2(s2, pk(__uint_as_float(ra[q]), __uint_as_float(ra[q + 1])),
+                               pk(__uint_as_float(rb[q]), __uint_as_float(rb[q + 1])));
+            out[k] = plo(r);
+            out[k + 1] = phi(r);
+        }
+    }
+}
+
 // spc_decode_list (list_engine.py:68-119) with one path on n = 8 (one element
 // per lane): tau = 1, i.e. the hard decision (:84-88) and one split (:97-112)
 // between keeping it and flipping the second least reliable position.
@@ -352,6 +388,24 @@ __global__ void __launch_bounds__(32 * kGrpWarps, 1) grp_kernel(rmfht::Params<fl
     const u32 pad = ((raw_saddr + 2047u) & ~2047u) - raw_saddr;
     float* const alpha_w = reinterpret_cast<float*>(graw + kGrpWarps * sizeof(WS) + pad + (size_t)wib * (4u << MM));
     const u32 asa = (u32)__cvta_generic_to_shared(alpha_w);
+    // tensor memory for the root's parked gathers: warp w owns lanes
+    // 32 (w % 4) .. + 31 and columns V (w / 4) .. + V - 1 of the CTA's 512
+    constexpr bool TPARK = RMFHT_TMEM_PARK != 0;
+    __shared__ u32 tmem_slot;
+    u32 tmem = 0;
+    if constexpr (TPARK) {
+        static_assert((kGrpWarps + 3) / 4 * V <= 512, "tensor-memory columns");
+        if (wib == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                             (u32)__cvta_generic_to_shared(&tmem_slot))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        tmem = tmem_slot + ((u32)(32 * (wib & 3)) << 16) + (u32)(V * (wib >> 2));
+    }
     const int M = prm.M;
     const long long rounds = prm.B * (long long)M / kItems;  // M % 4 == 0 (bind_one)
     const long long stride = (long long)gridDim.x * kGrpWarps;
@@ -443,22 +497,28 @@ __global__ void __launch_bounds__(32 * kGrpWarps, 1) grp_kernel(rmfht::Params<fl
             {
                 rmfht2::RootIdx<MM, kLpp, V> ri;
                 ri.build(ws.comp[g], u, asa);
+                if constexpr (TPARK) {
 #pragma unroll
-                for (int k = 0; k < VC; k++) xl[k] = f_op(lds_addr(ri.off(k)), lds_addr(ri.off(k + VC)));
-            }
-            int cb, cs;
-            const u32 bl = node<1, MM - 1>(xl, ws.wsp, lane, pm, cb, cs);
-            float xr[VC];
-            {
-                rmfht2::RootIdx<MM, kLpp, V> ri;
-                ri.build(ws.comp[g], u, asa);
-                float ga[VC], gb[VC];
+                    for (int k0 = 0; k0 < VC; k0 += 8) {
+                        float a[8], b[8];
 #pragma unroll
-                for (int k = 0; k < VC; k++) {
-                    ga[k] = lds_addr(ri.off(k));
-                    gb[k] = lds_addr(ri.off(k + VC));
+                        for (int i = 0; i < 8; i++) {
+                            a[i] = lds_addr(ri.off(k0 + i));
+                            b[i] = lds_addr(ri.off(k0 + i + VC));
+                        }
+                        rmfht2::tmem_st8(tmem + k0, a);
+                        rmfht2::tmem_st8(tmem + VC + k0, b);
+#pragma unroll
+                        for (int i = 0; i < 8; i++) xl[k0 + i] = f_op(a[i], b[i]);
+                    }
+                    rmfht2::tmem_wait_st();
+                } else {
+#pragma unroll
+                    for (int k = 0; k < VC; k++) xl[k] = f_op(lds_addr(ri.off(k)), lds_addr(ri.off(k + VC)));
                 }
-                // the frame LLRs are dead for this round: fetch the next round's if it is another frame
+            }
+            // the frame LLRs may be dead for this round: fetch the next round's if it is another frame
+            auto next_alpha = [&] {
                 const long long rn = r + stride;
                 if (rn < rounds) {
                     const long long fn = rn * kItems / M;
@@ -468,6 +528,23 @@ __global__ void __launch_bounds__(32 * kGrpWarps, 1) grp_kernel(rmfht::Params<fl
                         prefetch_alpha(fn);
                     }
                 }
+            };
+            if constexpr (TPARK) next_alpha();
+            int cb, cs;
+            const u32 bl = node<1, MM - 1>(xl, ws.wsp, lane, pm, cb, cs);
+            float xr[VC];
+            if constexpr (TPARK) {
+                g_after_fht_tmem<VC>(cb, cs, u, tmem, xr);
+            } else {
+                rmfht2::RootIdx<MM, kLpp, V> ri;
+                ri.build(ws.comp[g], u, asa);
+                float ga[VC], gb[VC];
+#pragma unroll
+                for (int k = 0; k < VC; k++) {
+                    ga[k] = lds_addr(ri.off(k));
+                    gb[k] = lds_addr(ri.off(k + VC));
+                }
+                next_alpha();
                 g_after_fht<VC>(cb, cs, u, ga, gb, xr);
             }
             int db, ds;
@@ -485,6 +562,11 @@ __global__ void __launch_bounds__(32 * kGrpWarps, 1) grp_kernel(rmfht::Params<fl
             __syncwarp();
         }
         if (lockstep) __syncthreads();
+    }
+    if constexpr (TPARK) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (wib == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_slot) : "memory");
     }
 }
 
