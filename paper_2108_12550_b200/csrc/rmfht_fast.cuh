@@ -1591,8 +1591,11 @@ __device__ __forceinline__ u64 node2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / 
 #endif
 template <int R, int MM, int L>
 __host__ __device__ constexpr bool tmem_park() {
-    // the root's left child is an FHT leaf (R == 2), 8 lanes per path, 32 slots per half
-    return RMFHT_TMEM_PARK && R == 2 && MM >= 3 && (32 / L) == 8 && ((1 << (MM - 1)) / (32 / L)) == 32;
+    // an internal root whose halves have a multiple of 8 slots per lane (the
+    // parked columns move in chunks of 8); 2 VC columns per warp, 7 warps per
+    // lane quadrant at most
+    constexpr int LPP = 32 / L, VC = (1 << (MM - 1)) / (LPP > 0 ? LPP : 1);
+    return RMFHT_TMEM_PARK && R > 1 && R < MM - 1 && L <= 32 && VC >= 8 && VC % 8 == 0 && 2 * VC * 8 <= 512;
 }
 __device__ __forceinline__ void tmem_st8(u32 taddr, const float* v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
@@ -1685,6 +1688,28 @@ __device__ __forceinline__ u64 root_node(Ctx2<R, MM, L>& cx, int8_t* lin, F&& al
         const int src1 = l1[p];
         const bool moved = __any_sync(kFull, src1 != p);
         const int from = src1 * C::LPP + u;
+        if constexpr (R - 1 != 1) {
+            // general left child: its hard decisions are the bits of bl
+#pragma unroll
+            for (int k0 = 0; k0 < VC; k0 += 8) {
+                u32 ra[8], rb[8];
+                tmem_ld8(cx.tmem + k0, ra);
+                tmem_ld8(cx.tmem + VC + k0, rb);
+                tmem_wait_ld16(ra, rb);
+                if (moved) {
+#pragma unroll
+                    for (int i = 0; i < 8; i++) {
+                        ra[i] = __shfl_sync(kFull, ra[i], from);
+                        rb[i] = __shfl_sync(kFull, rb[i], from);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    const float sg = ((bl >> (k0 + i)) & 1ull) ? -1.f : 1.f;
+                    xr[k0 + i] = __fmaf_rn(sg, __uint_as_float(ra[i]), __uint_as_float(rb[i]));
+                }
+            }
+        } else {
         constexpr int n = 1 << (MM - 1);
         const int bin = ws.sel_bin[p];
         const int sgn = ws.sel_w[p] < 0.f;
@@ -1721,6 +1746,7 @@ __device__ __forceinline__ u64 root_node(Ctx2<R, MM, L>& cx, int8_t* lin, F&& al
                 xr[k] = plo(r);
                 xr[k + 1] = phi(r);
             }
+        }
         }
     } else {
         RootIdx<MM, C::LPP, LV::V> ri;
@@ -1821,12 +1847,13 @@ __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Par
     constexpr bool ROOT_INTERNAL = !(R == 1 || R == MM - 1);
     // tensor memory for the root's parked gathers (tmem_park): the whole 512
     // columns (one CTA per SM); warp w owns lanes 32 (w % 4) .. + 31 (the
-    // quadrant a warp may access) and columns 64 (w / 4) .. + 63
+    // quadrant a warp may access) and 2 VC columns from 2 VC (w / 4)
     constexpr bool TPARK = PM && ROOT_INTERNAL && tmem_park<R, MM, L>();
     __shared__ u32 tmem_slot;
     cx.tmem = 0;
     if constexpr (TPARK) {
-        static_assert((nwarps + 3) / 4 * 64 <= 512, "tensor-memory columns");
+        constexpr int TCOLS = 2 * Lv<MM - 1, C::LPP>::V;  // columns per warp
+        static_assert((nwarps + 3) / 4 * TCOLS <= 512, "tensor-memory columns");
         if (warp == 0) {
             asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                              (u32)__cvta_generic_to_shared(&tmem_slot))
@@ -1836,7 +1863,7 @@ __global__ void __launch_bounds__(RMFHT_KERNEL2_LB, 1) decode_kernel2(rmfht::Par
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        cx.tmem = tmem_slot + ((u32)(32 * (warp & 3)) << 16) + (u32)(64 * (warp >> 2));
+        cx.tmem = tmem_slot + ((u32)(32 * (warp & 3)) << 16) + (u32)(TCOLS * (warp >> 2));
     }
     // items < 2^31 per launch (launch_fast splits larger batches)
     const int items = (int)prm.B * prm.M;
