@@ -320,6 +320,61 @@ __device__ __forceinline__ float lds_addr(u32 saddr) {
     return v;
 }
 
+// ------------------------------------------------- tensor-memory parking ----
+// The root's g (:104) needs the same 2 VC channel LLRs per lane that its f
+// (:100) gathered a whole left subtree earlier; there are no registers to
+// keep them and no shared memory left, so the kernel gathered them twice —
+// VC * 2 bank-conflicted LDS per lane, a fifth of the kernel's shared-memory
+// wavefronts.  Blackwell's tensor memory (256 KB per SM, unused by a kernel
+// without MMAs) holds them instead: f's gathers are stored with tcgen05.st
+// (32 lanes x 32-bit columns, a warp's own lane quadrant, its own column
+// block) and g reads them back with tcgen05.ld; when the left child re-ordered
+// the paths, the values come from the source path's lanes by shuffles.
+#ifndef RMFHT_NO_TMEM
+#define RMFHT_TMEM_PARK 1
+#else
+#define RMFHT_TMEM_PARK 0
+#endif
+template <int R, int MM, int L>
+__host__ __device__ constexpr bool tmem_park() {
+    // an internal root whose halves have a multiple of 8 slots per lane (the
+    // parked columns move in chunks of 8); 2 VC columns per warp, 7 warps per
+    // lane quadrant at most
+    constexpr int LPP = 32 / L, VC = (1 << (MM - 1)) / (LPP > 0 ? LPP : 1);
+    return RMFHT_TMEM_PARK && R > 1 && R < MM - 1 && L <= 32 && VC >= 8 && VC % 8 == 0 && 2 * VC * 8 <= 512;
+}
+__device__ __forceinline__ void tmem_st8(u32 taddr, const float* v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+                 "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+                 "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+                 "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_st1(u32 taddr, float v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(__float_as_uint(v)) : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(u32 taddr, u32* r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr)
+                 : "memory");
+}
+// the loaded registers may only be read after the wait: they pass through it
+__device__ __forceinline__ void tmem_wait_ld16(u32* a, u32* b) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
+                   "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]), "+r"(b[7])
+                 :
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld8(u32* a) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7])
+                 :
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 #ifdef RMFHT_STATS
 // diagnostic counters (tools/stats_run.py builds a separate library with them)
 __device__ unsigned long long g_stats[256];
@@ -1328,12 +1383,28 @@ __device__ __forceinline__ void perm_ext_root2(Ctx2<R, MM, L>& cx) {
         ws.cb[lane] = (int)d;
     }
     __syncwarp();
-#pragma unroll 1
-    for (int t = 0; t < 2 * L; t++) ws.lmp[t][lane] = lm_partial_root<C::NS>(cx.ach, (u32)ws.cb[t], lane, cx.alpha_saddr);
-    __syncwarp();
     float part[2 * L];
+    if constexpr (tmem_park<R, MM, L>() && 2 * L == 8) {
+        // the trials' lane partials wait in the warp's tensor-memory columns
+        // (idle until the root's f) instead of shared memory: the loop over
+        // the trials is not unrolled, a column address may be dynamic
+#pragma unroll 1
+        for (int t = 0; t < 2 * L; t++)
+            tmem_st1(cx.tmem + t, lm_partial_root<C::NS>(cx.ach, (u32)ws.cb[t], lane, cx.alpha_saddr));
+        tmem_wait_st();
+        u32 r8[8];
+        tmem_ld8(cx.tmem, r8);
+        tmem_wait_ld8(r8);
 #pragma unroll
-    for (int t = 0; t < 2 * L; t++) part[t] = ws.lmp[t][lane];
+        for (int t = 0; t < 8; t++) part[t] = __uint_as_float(r8[t]);
+    } else {
+#pragma unroll 1
+        for (int t = 0; t < 2 * L; t++)
+            ws.lmp[t][lane] = lm_partial_root<C::NS>(cx.ach, (u32)ws.cb[t], lane, cx.alpha_saddr);
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < 2 * L; t++) part[t] = ws.lmp[t][lane];
+    }
     int tri;
     const float tot = multi_tree<2 * L>(part, lane, &tri);
     if ((lane & (32 / (2 * L) - 1)) == 0) ws.lm[tri] = tot;
@@ -1573,52 +1644,6 @@ __device__ __forceinline__ u64 node2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / 
         return out;
     }
 }
-
-// ------------------------------------------------- tensor-memory parking ----
-// The root's g (:104) needs the same 2 VC channel LLRs per lane that its f
-// (:100) gathered a whole left subtree earlier; there are no registers to
-// keep them and no shared memory left, so the kernel gathered them twice —
-// VC * 2 bank-conflicted LDS per lane, a fifth of the kernel's shared-memory
-// wavefronts.  Blackwell's tensor memory (256 KB per SM, unused by a kernel
-// without MMAs) holds them instead: f's gathers are stored with tcgen05.st
-// (32 lanes x 32-bit columns, a warp's own lane quadrant, its own column
-// block) and g reads them back with tcgen05.ld; when the left child re-ordered
-// the paths, the values come from the source path's lanes by shuffles.
-#ifndef RMFHT_NO_TMEM
-#define RMFHT_TMEM_PARK 1
-#else
-#define RMFHT_TMEM_PARK 0
-#endif
-template <int R, int MM, int L>
-__host__ __device__ constexpr bool tmem_park() {
-    // an internal root whose halves have a multiple of 8 slots per lane (the
-    // parked columns move in chunks of 8); 2 VC columns per warp, 7 warps per
-    // lane quadrant at most
-    constexpr int LPP = 32 / L, VC = (1 << (MM - 1)) / (LPP > 0 ? LPP : 1);
-    return RMFHT_TMEM_PARK && R > 1 && R < MM - 1 && L <= 32 && VC >= 8 && VC % 8 == 0 && 2 * VC * 8 <= 512;
-}
-__device__ __forceinline__ void tmem_st8(u32 taddr, const float* v) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
-                 "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-                 "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-                 "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_ld8(u32 taddr, u32* r) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                 : "r"(taddr)
-                 : "memory");
-}
-// the loaded registers may only be read after the wait: they pass through it
-__device__ __forceinline__ void tmem_wait_ld16(u32* a, u32* b) {
-    asm volatile("tcgen05.wait::ld.sync.aligned;"
-                 : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
-                   "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]), "+r"(b[7])
-                 :
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // ------------------------------------------------------------ root node ----
 // Internal root (1 < r < m-1): the root vectors are never held; f (:100) and
