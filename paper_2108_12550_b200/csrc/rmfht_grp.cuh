@@ -453,13 +453,27 @@ __global__ void __launch_bounds__(32 * kGrpWarps, 1) grp_kernel(rmfht::Params<fl
                 ws.dir[lane] = (int)rmfht2::icol_apply<MM>(maps[i * kMaps], (u32)maps[i * kMaps + 1 + t].icol[MM - 1]);
             }
             __syncwarp();
-#pragma unroll 1
-            for (int t = 0; t < 2 * kItems; t++) ws.lmp[t][lane] = rmfht2::lm_partial_root<NS>(ach, (u32)ws.dir[t], lane, asa);
-            __syncwarp();
             {
                 float part[2 * kItems];
+                if constexpr (TPARK) {
+                    // the lane partials wait in the warp's tensor-memory columns (idle until the root's f)
+#pragma unroll 1
+                    for (int t = 0; t < 2 * kItems; t++)
+                        rmfht2::tmem_st1(tmem + t, rmfht2::lm_partial_root<NS>(ach, (u32)ws.dir[t], lane, asa));
+                    rmfht2::tmem_wait_st();
+                    u32 r8[8];
+                    rmfht2::tmem_ld8(tmem, r8);
+                    rmfht2::tmem_wait_ld8(r8);
 #pragma unroll
-                for (int t = 0; t < 2 * kItems; t++) part[t] = ws.lmp[t][lane];
+                    for (int t = 0; t < 8; t++) part[t] = __uint_as_float(r8[t]);
+                } else {
+#pragma unroll 1
+                    for (int t = 0; t < 2 * kItems; t++)
+                        ws.lmp[t][lane] = rmfht2::lm_partial_root<NS>(ach, (u32)ws.dir[t], lane, asa);
+                    __syncwarp();
+#pragma unroll
+                    for (int t = 0; t < 2 * kItems; t++) part[t] = ws.lmp[t][lane];
+                }
                 int tri;
                 const float tot = rmfht2::multi_tree<2 * kItems>(part, lane, &tri);
                 if ((lane & (32 / (2 * kItems) - 1)) == 0) ws.lm[tri] = tot;
