@@ -1384,7 +1384,7 @@ __device__ __forceinline__ void perm_ext_root2(Ctx2<R, MM, L>& cx) {
     }
     __syncwarp();
     float part[2 * L];
-    if constexpr (tmem_park<R, MM, L>() && 2 * L == 8) {
+    if constexpr (tmem_park<R, MM, L>() && (2 * L) % 8 == 0 && 2 * L <= 2 * Lv<MM - 1, C::LPP>::V) {
         // the trials' lane partials wait in the warp's tensor-memory columns
         // (idle until the root's f) instead of shared memory: the loop over
         // the trials is not unrolled, a column address may be dynamic
@@ -1392,11 +1392,14 @@ __device__ __forceinline__ void perm_ext_root2(Ctx2<R, MM, L>& cx) {
         for (int t = 0; t < 2 * L; t++)
             tmem_st1(cx.tmem + t, lm_partial_root<C::NS>(cx.ach, (u32)ws.cb[t], lane, cx.alpha_saddr));
         tmem_wait_st();
-        u32 r8[8];
-        tmem_ld8(cx.tmem, r8);
-        tmem_wait_ld8(r8);
 #pragma unroll
-        for (int t = 0; t < 8; t++) part[t] = __uint_as_float(r8[t]);
+        for (int t0 = 0; t0 < 2 * L; t0 += 8) {
+            u32 r8[8];
+            tmem_ld8(cx.tmem + t0, r8);
+            tmem_wait_ld8(r8);
+#pragma unroll
+            for (int t = 0; t < 8; t++) part[t0 + t] = __uint_as_float(r8[t]);
+        }
     } else {
 #pragma unroll 1
         for (int t = 0; t < 2 * L; t++)
