@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include "rmfht_kernels.cuh"
+#include "rmfht_fast.cuh"  // tensor-memory parking helpers
 
 namespace rmfht_pair {
 
@@ -459,6 +460,23 @@ __global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<
     const int lane = threadIdx.x & 31, wib = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // provably warp-uniform
     const int M = prm.M, FPW = 16 / M;  // frames per warp (M divides 16)
     float* fw = fr + (size_t)wib * FPW * N;
+    // tensor memory for the root's gathers between f and g (rmfht2::tmem_park):
+    // N columns per thread, warp w in lanes 32 (w % 4) .. + 31, columns N (w / 4) ..
+    constexpr bool TPARK = RMFHT_TMEM_PARK != 0 && H % 8 == 0 && (kPairWarps + 3) / 4 * N <= 512;
+    __shared__ u32 tmem_slot;
+    u32 tmem = 0;
+    if constexpr (TPARK) {
+        if (wib == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                             (u32)__cvta_generic_to_shared(&tmem_slot))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        tmem = tmem_slot + ((u32)(32 * (wib & 3)) << 16) + (u32)(N * (wib >> 2));
+    }
     const int q = lane & 1, it = lane >> 1;
     const long long items = prm.B * (long long)M;
     const long long warps_total = (items + 15) / 16;
@@ -571,10 +589,43 @@ __global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<
         tc.build(comp);
         tc.rebase(abase);
         float xl[H];
+        if constexpr (TPARK) {
+            // the gathered halves wait in tensor memory for g (column j: lower half, H + j: upper)
 #pragma unroll
-        for (int j = 0; j < H; j++) xl[j] = f_op(lds(tc.at(j)), lds(tc.at(j + H)));
+            for (int j0 = 0; j0 < H; j0 += 8) {
+                float a[8], b[8];
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    a[i] = lds(tc.at(j0 + i));
+                    b[i] = lds(tc.at(j0 + i + H));
+                }
+                rmfht2::tmem_st8(tmem + j0, a);
+                rmfht2::tmem_st8(tmem + H + j0, b);
+#pragma unroll
+                for (int i = 0; i < 8; i++) xl[j0 + i] = f_op(a[i], b[i]);
+            }
+            rmfht2::tmem_wait_st();
+        } else {
+#pragma unroll
+            for (int j = 0; j < H; j++) xl[j] = f_op(lds(tc.at(j)), lds(tc.at(j + H)));
+        }
         int l1;
         const BitsT<MM - 1> bl = node<1, MM - 1>(xl, nd, q, &l1);  // :101 (RM(1, m-1): FHT)
+        float xr[H];
+        if constexpr (TPARK) {
+            // g on the parked gathers of slot l1 (:102-104): mine, or the partner thread's
+#pragma unroll
+            for (int j0 = 0; j0 < H; j0 += 8) {
+                u32 ra[8], rb[8];
+                rmfht2::tmem_ld8(tmem + j0, ra);
+                rmfht2::tmem_ld8(tmem + H + j0, rb);
+                rmfht2::tmem_wait_ld16(ra, rb);
+#pragma unroll
+                for (int i = 0; i < 8; i++)
+                    xr[j0 + i] = g_op(__uint_as_float(from_slot(ra[i], q, l1)), __uint_as_float(from_slot(rb[i], q, l1)),
+                                      (int)((bl >> (j0 + i)) & 1));
+            }
+        } else {
         // g through the composite of slot l1 (:102-104)
         InvTab<MM> tg;
         {
@@ -585,9 +636,9 @@ __global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<
             tg.build(cs);
             tg.rebase(abase);
         }
-        float xr[H];
 #pragma unroll
         for (int j = 0; j < H; j++) xr[j] = g_op(lds(tg.at(j)), lds(tg.at(j + H)), (int)((bl >> j) & 1));
+        }
         int l2;
         const BitsT<MM - 1> br = node<2, MM - 1>(xr, nd, q, &l2);  // :105
         const BitsT<MM - 1> blm = from_slot(bl, q, l2);
@@ -719,6 +770,11 @@ __global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<
             prm.path[fidx] = best;
         }
         __syncthreads();
+    }
+    if constexpr (TPARK) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (wib == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_slot) : "memory");
     }
 }
 
