@@ -330,6 +330,12 @@ __device__ __forceinline__ float lds_addr(u32 saddr) {
 // (32 lanes x 32-bit columns, a warp's own lane quadrant, its own column
 // block) and g reads them back with tcgen05.ld; when the left child re-ordered
 // the paths, the values come from the source path's lanes by shuffles.
+#ifndef RMFHT_XPARK
+#define RMFHT_XPARK 1
+#endif
+#ifndef RMFHT_XPARK_MINV
+#define RMFHT_XPARK_MINV 32
+#endif
 #ifndef RMFHT_NO_TMEM
 #define RMFHT_TMEM_PARK 1
 #else
@@ -1579,7 +1585,40 @@ __device__ __forceinline__ u64 node2(Ctx2<R, MM, L>& cx, float (&x)[Lv<SS, 32 / 
             const float o = __shfl_down_sync(kFull, x[0], h);
             xl[0] = (u < h) ? f_op(x[0], o) : 0.f;
         }
+        // An internal node's own vector waits in the warp's tensor-memory block
+        // (free after the root's g: for R == 2 every left child is a leaf and
+        // these nodes all lie in the root's right subtree) while its left
+        // child runs: the FHT leaf then has the registers to itself.
+        constexpr bool XPARK = RMFHT_XPARK && tmem_park<R, MM, L>() && R == 2 && SS < MM && LV::full && V % 8 == 0 &&
+                               V >= RMFHT_XPARK_MINV;
+        if constexpr (XPARK) {
+#pragma unroll
+            for (int k0 = 0; k0 < V; k0 += 8) tmem_st8(cx.tmem + k0, &x[k0]);
+            tmem_wait_st();
+        }
         const u64 bl = node2<R, MM, L, RR - 1, SS - 1, SPINE>(cx, xl, l1);   // :101
+        if constexpr (XPARK) {
+            if constexpr (V == 8) {
+                u32 ra[8];
+                tmem_ld8(cx.tmem, ra);
+                tmem_wait_ld8(ra);
+#pragma unroll
+                for (int i = 0; i < 8; i++) x[i] = __uint_as_float(ra[i]);
+            } else {
+#pragma unroll
+                for (int k0 = 0; k0 < V; k0 += 16) {
+                    u32 ra[8], rb[8];
+                    tmem_ld8(cx.tmem + k0, ra);
+                    tmem_ld8(cx.tmem + k0 + 8, rb);
+                    tmem_wait_ld16(ra, rb);
+#pragma unroll
+                    for (int i = 0; i < 8; i++) {
+                        x[k0 + i] = __uint_as_float(ra[i]);
+                        x[k0 + 8 + i] = __uint_as_float(rb[i]);
+                    }
+                }
+            }
+        }
         // alphas = alphas[lin1] (:102)
         const int src1 = l1[p];
         const bool moved = __any_sync(kFull, src1 != p);
