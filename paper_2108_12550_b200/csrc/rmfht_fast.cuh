@@ -2072,6 +2072,14 @@ __global__ void __launch_bounds__(256) reduce_kernel2(rmfht::Params<float> prm, 
     const long long f = (long long)blockIdx.x * 8 + warp;
     if (f >= prm.B) return;
     const int M = prm.M;
+    // the frame's LLRs (for the reported pm) do not depend on the winner:
+    // in flight while the attempt records are reduced
+    float fll[NW];
+    {
+        const float* fl0 = prm.llr + (size_t)f * N;
+#pragma unroll
+        for (int t = 0; t < NW; t++) fll[t] = __ldg(fl0 + t * 32 + lane);
+    }
     // first minimum over (pm, attempt)
     float bp = 0.f;
     int ba = -1;
@@ -2118,13 +2126,12 @@ __global__ void __launch_bounds__(256) reduce_kernel2(rmfht::Params<float> prm, 
         // reported pm: the decided codeword's metric from the channel LLRs
         // (rmfht::CorrPm); the accumulated h.pm selected the attempt
         rmfht::CorrPm corr;
-        const float* fl = prm.llr + (size_t)f * N;
 #pragma unroll
         for (int t = 0; t < NW; t++) {
             const u32 i = (u32)(t * 32 + lane);
             const u32 e = fm.b ^ lin_apply<MM>(fm.col, i);
             const int bit = (int)((sbits[warp][e % LPP] >> (e / LPP)) & 1ull);
-            corr.add(__ldg(fl + i), bit);
+            corr.add(fll[t], bit);
             const u32 word = __ballot_sync(kFull, bit);
             if (lane == t) myword = word;
         }
