@@ -228,7 +228,10 @@ int launch_pair(const rmfht_plan* p, const void* llr, const uint16_t* maps, uint
 
 template <int MM>
 int prepare_pair(rmfht_plan* p) {
-    const size_t smem = (size_t)rmfht_pair::kPairWarps * (16 / p->M) * (1u << MM) * sizeof(float) +
+    // M >= 4: two frame buffers and two record buffers per warp (the next round's are prefetched)
+    const size_t frames = (size_t)rmfht_pair::kPairWarps * (16 / p->M) * (1u << MM) * sizeof(float);
+    const size_t records = (size_t)rmfht_pair::kPairWarps * 16 * 6 * (2 * MM + 2) * sizeof(uint16_t);
+    const size_t smem = (p->M >= 4 ? 2 * frames + 2 * records : frames) +
                         (size_t)(4u << MM);  // alignment pad of the frame buffers
     cudaError_t a = cudaFuncSetAttribute(rmfht_pair::pair_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);

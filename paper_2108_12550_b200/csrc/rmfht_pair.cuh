@@ -42,6 +42,9 @@ constexpr int L = 2;  // list size (paths per item)
 #define RMFHT_PAIR_WARPS 16  // lock-stepped warps per CTA (128 registers, one CTA per SM)
 #endif
 constexpr int kPairWarps = RMFHT_PAIR_WARPS;
+#ifndef RMFHT_PAIR_PREFETCH
+#define RMFHT_PAIR_PREFETCH 1
+#endif
 
 // |x| as an operand modifier.  It differs from the reference's x < 0 ? -x : x
 // only in the sign of a zero, which no comparison, sum or decision sees.
@@ -459,7 +462,19 @@ __global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<
     float* const fr = reinterpret_cast<float*>(fraw + ((((rs + 4 * N - 1) / (4 * N)) * (4 * N)) - rs));
     const int lane = threadIdx.x & 31, wib = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // provably warp-uniform
     const int M = prm.M, FPW = 16 / M;  // frames per warp (M divides 16)
-    float* fw = fr + (size_t)wib * FPW * N;
+    // PREF: the next round's frames and map records are in flight (cp.async,
+    // double buffers) while this round decodes; needs 16-byte aligned sources
+    // and whole 16-byte records per item (m = 7)
+    constexpr int RECB = S * REC * 2;  // record bytes per item
+    constexpr bool PREFC = RMFHT_PAIR_PREFETCH != 0 && RECB % 16 == 0;
+    // (M >= 4: at most four frames per warp, so the double buffers fit; prepare_pair sizes them)
+    const bool pref = PREFC && prm.M >= 4 && (reinterpret_cast<uintptr_t>(prm.llr) & 15u) == 0 &&
+                      (reinterpret_cast<uintptr_t>(prm.maps) & 15u) == 0;
+    const size_t fbuf = (size_t)kPairWarps * FPW * N;  // floats of one frame buffer (all warps)
+    float* const fw0 = fr + (size_t)wib * FPW * N;  // the warp's frames in buffer 0
+    float* fw = fw0;
+    uint16_t* const recs0 = reinterpret_cast<uint16_t*>(fr + 2 * fbuf) + (size_t)wib * 16 * S * REC;
+    const size_t rbuf = (size_t)kPairWarps * 16 * S * REC;  // uint16 of one record buffer (all warps)
     // tensor memory for the root's gathers between f and g (rmfht2::tmem_park):
     // N columns per thread, warp w in lanes 32 (w % 4) .. + 31, columns N (w / 4) ..
     constexpr bool TPARK = RMFHT_TMEM_PARK != 0 && H % 8 == 0 && (kPairWarps + 3) / 4 * N <= 512;
@@ -485,6 +500,23 @@ __global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<
     // stream (free-running warps thrashed the instruction caches: 39%
     // no_instructions stalls at 12 warps per SM)
     const int nwb = blockDim.x >> 5;
+    auto prefetch = [&](long long wgn, int buf) {
+        if (wgn >= warps_total) return;
+        const long long i0 = wgn * 16, fn = i0 / M;
+        const u32 fsa = (u32)__cvta_generic_to_shared(fw0 + buf * fbuf);
+        for (int i = lane; i < FPW * N / 4; i += 32) {
+            const long long f = fn + (i * 4) / N;
+            if (f < prm.B) rmfht2::cp_async16(fsa + 16u * i, reinterpret_cast<const float4*>(prm.llr + f * N) + (i % (N / 4)));
+        }
+        const long long left = items - i0;
+        const int nb = (int)(left < 16 ? left : 16) * RECB / 16;  // 16-byte chunks of the round's records
+        const u32 rsa = (u32)__cvta_generic_to_shared(recs0 + buf * rbuf);
+        const char* gr = reinterpret_cast<const char*>(prm.maps + (size_t)i0 * S * REC);
+        for (int i = lane; i < nb; i += 32) rmfht2::cp_async16(rsa + 16u * i, gr + 16 * i);
+        rmfht2::cp_async_commit();
+    };
+    int cur = 0;
+    if (pref) prefetch((long long)blockIdx.x * nwb + wib, 0);
     for (long long r0 = (long long)blockIdx.x * nwb; r0 < warps_total; r0 += (long long)gridDim.x * nwb) {
         const long long wg = r0 + wib;
         if (wg >= warps_total) {
@@ -492,6 +524,12 @@ __global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<
             continue;
         }
         const long long item0 = wg * 16, f0 = item0 / M;
+        if (pref) {
+            rmfht2::cp_async_wait_all();
+            __syncwarp();
+            fw = fw0 + cur * fbuf;
+            prefetch(wg + (long long)gridDim.x * nwb, cur ^ 1);
+        } else {
         // the warp's frames into shared memory (coalesced)
         __syncwarp();
         for (int i = lane; i < FPW * N / 4; i += 32) {
@@ -501,6 +539,7 @@ __global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<
             reinterpret_cast<float4*>(fw)[i] = v;
         }
         __syncwarp();
+        }
         const long long item = item0 + it;
         const bool live = item < items;
         const long long fidx = live ? item / M : f0;
@@ -508,7 +547,8 @@ __global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<
         const float* alpha = fw + (fidx - f0) * N;
         const u32 abase = (u32)__cvta_generic_to_shared(alpha);
         // this thread's maps: root map q, trial maps q and q + 2 (both permute path q)
-        const uint16_t* rec = prm.maps + (size_t)(live ? item : item0) * S * REC;
+        const uint16_t* rec = pref ? recs0 + cur * rbuf + (size_t)(live ? it : 0) * S * REC
+                                   : prm.maps + (size_t)(live ? item : item0) * S * REC;
         Map<MM> root, t0, t1;
         root.load(rec + q * REC);
         t0.load(rec + (L + q) * REC);
@@ -769,6 +809,7 @@ __global__ void __launch_bounds__(32 * kPairWarps, 1) pair_kernel(rmfht::Params<
             prm.attempt[fidx] = at;
             prm.path[fidx] = best;
         }
+        cur ^= 1;
         __syncthreads();
     }
     if constexpr (TPARK) {
